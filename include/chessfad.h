@@ -1,0 +1,119 @@
+/*
+ * chessfad.h -- C-ABI of the B200-native batched FP64 Hessian-vector product library
+ * (libchessfad.so), a from-scratch implementation of the data-parallel hot path of
+ * CHESSFAD (arXiv 2410.22575).
+ *
+ * Citations: PAPER.md / SPEC.md line numbers of the reference text (DESIGN.md lists the
+ * section each belongs to).  All floating point is IEEE FP64 (the paper's
+ * `double v[2*csize+2]`).
+ *
+ * Conventions shared by every entry point
+ *   func     test function id (definitions):
+ *              CHESSFAD_ROSENBROCK      sum 100(y_{i+1}-y_i^2)^2 + (1-y_i)^2, needs n >= 2
+ *              CHESSFAD_ACKLEY          -20 exp(-0.2 sqrt(S/n)) - exp(sum cos(2 pi y)/n) + 20 + e
+ *              CHESSFAD_FLETCHER_POWELL sum_k (E*_k - sum_j A_kj sin y_j + B_kj cos y_j)^2
+ *              CHESSFAD_PRODSUM         sum y_i y_{i+1} (count calibration), needs n >= 2
+ *   n        number of variables, >= 1
+ *   csize    chunk size C of hDual<C>: 1 <= C <= n and C | n
+ *            (the paper assumes exact division)
+ *   m        number of points (instances); m == 0 is an empty no-op
+ *   points   m x n FP64 row-major, point e at points[e*n .. e*n+n)
+ *   vecs     m x n FP64 row-major, multiplicand of point e
+ *   params   Fletcher-Powell only, else ignored (may be NULL): 2n^2+n FP64
+ *            [A (n x n row-major) | B (n x n row-major) | E* (n)]
+ *   stream   a cudaStream_t passed as void* (NULL = legacy default stream)
+ *   Memory is owned by the caller.  Outputs must not alias inputs.  Outputs are fully
+ *   overwritten.  NaN/Inf propagate and are not errors:
+ *   Ackley at the origin yields NaN derivatives by design.
+ *   The library never aborts, never throws across the ABI, allocates nothing that
+ *   outlives a call, and keeps no global mutable state beyond one-time kernel attributes.
+ *   Calls on distinct streams are thread-safe.
+ */
+#ifndef CHESSFAD_H
+#define CHESSFAD_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum chessfad_func {
+  CHESSFAD_ROSENBROCK = 0,
+  CHESSFAD_ACKLEY = 1,
+  CHESSFAD_FLETCHER_POWELL = 2,
+  CHESSFAD_PRODSUM = 3
+};
+
+enum chessfad_status {
+  CHESSFAD_OK = 0,
+  CHESSFAD_ERR_ARG = 1,         /* n < 1, m < 0, or a NULL data pointer with m > 0 */
+  CHESSFAD_ERR_CHUNK = 2,       /* csize < 1, csize > n, or n % csize != 0 */
+  CHESSFAD_ERR_FUNC = 3,        /* unknown func, n < 2 for Rosenbrock/prodsum, NULL params for F3 */
+  CHESSFAD_ERR_UNSUPPORTED = 4, /* (func, n, csize) outside the compiled set (chessfad_is_supported) */
+  CHESSFAD_ERR_CUDA = 5         /* a CUDA runtime error (launch, copy, allocation) */
+};
+
+/*
+ * Batched Hessian-vector product, Alg 7 CHESS-VEC over m points:
+ *   out[e*n + i] = sum_j  d2f/dx_i dx_j (points[e]) * vecs[e*n + j]
+ * computed row by row and chunk by chunk with hDual<csize> forward propagation
+ * (Alg 4 CHUNK-INIT; Fig. 1 rules), never storing H
+ * (PAPER.md:246).  points, vecs, out (m x n) and params are DEVICE pointers.
+ * Asynchronous on `stream`: no host synchronisation; results are valid once the caller
+ * synchronises the stream.  Returns a chessfad_status.
+ */
+int chessfad_hvp_batch(int func, int n, int csize, int64_t m, const double *points, const double *vecs,
+                       double *out, const double *params, void *stream);
+
+/*
+ * Batched dense Hessian, Alg 5 CHUNK-HESS:
+ *   hess[e*n*n + i*n + j] = d2f/dx_i dx_j (points[e])
+ * every (i, j) computed (not mirrored), n^2/csize evaluations per point.
+ * DEVICE pointers; hess is m x n x n.  Asynchronous on `stream`.
+ */
+int chessfad_hessian_batch(int func, int n, int csize, int64_t m, const double *points, double *hess,
+                           const double *params, void *stream);
+
+/*
+ * End-to-end variant of chessfad_hvp_batch on HOST buffers: points, vecs, out (m x n) and
+ * params are HOST pointers (pinned memory gives copy/compute overlap; pageable memory
+ * works but serialises).  The batch is split into pieces of `piece_points` points
+ * (<= 0: library default) that flow H2D -> kernel -> D2H through two CUDA streams so
+ * that copies overlap computation.  Device scratch is allocated stream-ordered and freed
+ * before return.  SYNCHRONOUS: returns after `out` holds the result.  `stream` orders the
+ * work after prior work on it (NULL = legacy default stream).
+ */
+int chessfad_hvp_batch_host(int func, int n, int csize, int64_t m, const double *points, const double *vecs,
+                            double *out, const double *params, int64_t piece_points, void *stream);
+
+/* 1 if (func, n, csize) has a compiled kernel, else 0 (argument errors also give 0). */
+int chessfad_is_supported(int func, int n, int csize);
+
+/* Static description of a status code. */
+const char *chessfad_status_string(int status);
+
+/*
+ * Model FLOPs per point of one call: the paper's
+ * §V count extended to all hDual ops with hh* = 10C+4 (6C+3 mul +
+ * 4C+1 add, Fig. 1 code), hh+ = s* = 2C+2, s+ = 1, unary = 4C+2 (g, g', g'' count 0),
+ * times n^2/C evaluations, plus the 2n^2 of the HVP dot when hessian == 0.
+ * Returns -1 on invalid arguments.
+ */
+double chessfad_model_flops_per_point(int func, int n, int csize, int hessian);
+
+/*
+ * FP64 pipe probe: launches `blocks` x 256 threads, each running `iters` iterations of one
+ * DFMA on each of 8 independent chains, and writes one double per thread to `sink`
+ * (DEVICE, blocks*256 doubles) so nothing is dead.  FLOPs per launch =
+ * blocks * 256 * iters * 16.  Used by bench.py to measure the attainable FP64 rate.
+ */
+int chessfad_fp64_probe(int blocks, int64_t iters, double *sink, void *stream);
+
+/* Library version string. */
+const char *chessfad_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHESSFAD_H */

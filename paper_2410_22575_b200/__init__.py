@@ -1,0 +1,162 @@
+"""chessfad-b200: B200-native batched FP64 Hessian-vector products (CHESSFAD, arXiv 2410.22575).
+
+Thin Python binding over the C-ABI of ``libchessfad.so`` (``include/chessfad.h``):
+argument marshalling only -- every step of the hot path runs in the library's CUDA
+kernels.  PyTorch supplies device memory and streams.  There is no CPU fallback: if the
+library cannot be loaded the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libchessfad.so")
+
+ROSENBROCK, ACKLEY, FLETCHER_POWELL, PRODSUM = 0, 1, 2, 3
+FUNCS = {"rosenbrock": ROSENBROCK, "ackley": ACKLEY, "fletcher_powell": FLETCHER_POWELL, "prodsum": PRODSUM}
+STATUS = {0: "CHESSFAD_OK", 1: "CHESSFAD_ERR_ARG", 2: "CHESSFAD_ERR_CHUNK", 3: "CHESSFAD_ERR_FUNC",
+          4: "CHESSFAD_ERR_UNSUPPORTED", 5: "CHESSFAD_ERR_CUDA"}
+EXPORTS = ["chessfad_hvp_batch", "chessfad_hessian_batch", "chessfad_hvp_batch_host", "chessfad_is_supported",
+           "chessfad_status_string", "chessfad_model_flops_per_point", "chessfad_fp64_probe", "chessfad_version"]
+
+_lock = threading.Lock()
+_lib = None
+
+
+class ChessfadError(RuntimeError):
+    def __init__(self, status: int, msg: str = ""):
+        self.status = status
+        super().__init__(f"{STATUS.get(status, status)}{': ' + msg if msg else ''}")
+
+
+def load(build_if_missing: bool = True):
+    """Load libchessfad.so (building it in-tree with nvcc if it is missing or stale)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        from . import build as _build
+        if build_if_missing and not _build.up_to_date():
+            _build.build()
+        if not os.path.exists(LIB_PATH):
+            raise ChessfadError(5, f"{LIB_PATH} not built; run paper_2410_22575_b200/build.py")
+        lib = ctypes.CDLL(LIB_PATH)
+        i32, i64, dbl, vp = ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
+        sig = {
+            "chessfad_hvp_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
+            "chessfad_hessian_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
+            "chessfad_hvp_batch_host": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, i64, vp]),
+            "chessfad_is_supported": (i32, [i32, i32, i32]),
+            "chessfad_status_string": (ctypes.c_char_p, [i32]),
+            "chessfad_model_flops_per_point": (dbl, [i32, i32, i32, i32]),
+            "chessfad_fp64_probe": (i32, [i32, i64, vp, vp]),
+            "chessfad_version": (ctypes.c_char_p, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib
+        return lib
+
+
+def _func(f) -> int:
+    return FUNCS[f] if isinstance(f, str) else int(f)
+
+
+def _check(st: int):
+    if st != 0:
+        raise ChessfadError(st, load().chessfad_status_string(st).decode())
+
+
+def _stream_ptr(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev(t, name, shape=None):
+    import torch
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        raise TypeError(f"{name} must be a contiguous float64 CUDA tensor")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def hvp_batch(func, points, vecs, csize: int, params=None, out=None, stream=None):
+    """out[e] = Hess f(points[e]) @ vecs[e] for every row e (Alg 7, batched).
+
+    points, vecs: (m, n) float64 CUDA tensors; params: (2n^2+n,) float64 CUDA tensor for
+    Fletcher-Powell.  Asynchronous on `stream` (default: torch's current stream)."""
+    import torch
+    m, n = points.shape
+    if out is None:
+        out = torch.empty_like(points)
+    st = load().chessfad_hvp_batch(_func(func), n, csize, m, _dev(points, "points"), _dev(vecs, "vecs", (m, n)),
+                                   _dev(out, "out", (m, n)), _dev(params, "params"), _stream_ptr(stream))
+    _check(st)
+    return out
+
+
+def hessian_batch(func, points, csize: int, params=None, out=None, stream=None):
+    """hess[e] = Hess f(points[e]), every entry computed (Alg 5, batched): (m, n, n)."""
+    import torch
+    m, n = points.shape
+    if out is None:
+        out = torch.empty((m, n, n), dtype=torch.float64, device=points.device)
+    st = load().chessfad_hessian_batch(_func(func), n, csize, m, _dev(points, "points"), _dev(out, "hess", (m, n, n)),
+                                       _dev(params, "params"), _stream_ptr(stream))
+    _check(st)
+    return out
+
+
+def _host_ptr(x, name, writable=False):
+    import numpy as np
+    import torch
+    if x is None:
+        return None, None
+    if isinstance(x, torch.Tensor):
+        if x.is_cuda or x.dtype != torch.float64 or not x.is_contiguous():
+            raise TypeError(f"{name} must be a contiguous float64 CPU tensor")
+        return ctypes.c_void_p(x.data_ptr()), x
+    a = np.asarray(x)
+    if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"] or (writable and not a.flags["WRITEABLE"]):
+        raise TypeError(f"{name} must be a contiguous writable float64 array")
+    return ctypes.c_void_p(a.ctypes.data), a
+
+
+def hvp_batch_host(func, points, vecs, csize: int, params=None, out=None, piece_points: int = 0, stream=None):
+    """End-to-end HVP on HOST buffers (numpy arrays or CPU tensors, ideally pinned):
+    H2D copies, kernels and D2H copies pipelined over two streams; synchronous."""
+    import torch
+    m, n = points.shape
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float64, pin_memory=torch.cuda.is_available())
+    pp, _ = _host_ptr(points, "points")
+    pv, _ = _host_ptr(vecs, "vecs")
+    po, _ = _host_ptr(out, "out", writable=True)
+    ppar, _ = _host_ptr(params, "params")
+    st = load().chessfad_hvp_batch_host(_func(func), n, csize, m, pp, pv, po, ppar, piece_points, _stream_ptr(stream))
+    _check(st)
+    return out
+
+
+def is_supported(func, n: int, csize: int) -> bool:
+    return bool(load().chessfad_is_supported(_func(func), n, csize))
+
+
+def model_flops_per_point(func, n: int, csize: int, hessian: bool = False) -> float:
+    return float(load().chessfad_model_flops_per_point(_func(func), n, csize, int(hessian)))
+
+
+def fp64_probe(blocks: int, iters: int, sink, stream=None):
+    _check(load().chessfad_fp64_probe(blocks, iters, _dev(sink, "sink"), _stream_ptr(stream)))
+
+
+def version() -> str:
+    return load().chessfad_version().decode()

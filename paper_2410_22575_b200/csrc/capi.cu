@@ -1,0 +1,243 @@
+// capi.cu -- the C-ABI of libchessfad.so (include/chessfad.h): argument validation,
+// dispatch on (func, csize) to the compiled kernel set, the host-buffer pipeline, the
+// model-FLOP count and the FP64 probe.  Host code only launches kernels; no compute here.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "../../include/chessfad.h"
+#include "launch.cuh"
+
+using namespace chessfad;
+
+namespace {
+
+constexpr int kMaxNReg = 256;  // register-hDual path: 3*n*33*8 B of shared memory per CTA
+constexpr int kMaxNF3 = 128;   // F3 path: per-thread R0/R1 scratch of 128 doubles
+
+bool reg_chunk_compiled(int C) { return C == 1 || C == 2 || C == 4 || C == 8 || C == 16 || C == 32; }
+
+int validate(int func, int n, int csize, int64_t m, bool need_params_ptr, const void* params,
+             const void* p1, const void* p2, const void* p3) {
+  if (n < 1 || m < 0) return CHESSFAD_ERR_ARG;
+  if (m > 0 && (!p1 || !p2 || (p3 == nullptr && need_params_ptr))) return CHESSFAD_ERR_ARG;
+  if (csize < 1 || csize > n || n % csize != 0) return CHESSFAD_ERR_CHUNK;
+  switch (func) {
+    case CHESSFAD_ROSENBROCK:
+    case CHESSFAD_PRODSUM:
+      if (n < 2) return CHESSFAD_ERR_FUNC;
+      break;
+    case CHESSFAD_ACKLEY:
+      break;
+    case CHESSFAD_FLETCHER_POWELL:
+      if (!params) return CHESSFAD_ERR_FUNC;
+      break;
+    default:
+      return CHESSFAD_ERR_FUNC;
+  }
+  return CHESSFAD_OK;
+}
+
+int supported(int func, int n, int csize) {
+  if (func == CHESSFAD_FLETCHER_POWELL) return n <= kMaxNF3;
+  return n <= kMaxNReg && reg_chunk_compiled(csize);
+}
+
+// largest power of two <= 16 that divides n: the F3 k-block
+int f3_kb(int n) {
+  int kb = 16;
+  while (n % kb) kb >>= 1;
+  return kb;
+}
+
+template <bool HESS>
+cudaError_t dispatch_reg(int func, int C, const BatchArgs& a, cudaStream_t s) {
+#define CHF_CASE_C(F)                                  \
+  switch (C) {                                         \
+    case 1: return launch_reg<F, 1, HESS>(a, s);       \
+    case 2: return launch_reg<F, 2, HESS>(a, s);       \
+    case 4: return launch_reg<F, 4, HESS>(a, s);       \
+    case 8: return launch_reg<F, 8, HESS>(a, s);       \
+    case 16: return launch_reg<F, 16, HESS>(a, s);     \
+    case 32: return launch_reg<F, 32, HESS>(a, s);     \
+  }                                                    \
+  break;
+  switch (func) {
+    case CHESSFAD_ROSENBROCK: CHF_CASE_C(FUNC_ROSENBROCK)
+    case CHESSFAD_ACKLEY: CHF_CASE_C(FUNC_ACKLEY)
+    case CHESSFAD_PRODSUM: CHF_CASE_C(FUNC_PRODSUM)
+  }
+#undef CHF_CASE_C
+  return cudaErrorInvalidValue;
+}
+
+template <bool HESS>
+cudaError_t dispatch_f3(const BatchArgs& a, cudaStream_t s) {
+  const bool ab_smem = a.n <= 32;
+#define CHF_CASE_KB(KB) \
+  case KB: return ab_smem ? launch_f3<KB, HESS, true>(a, s) : launch_f3<KB, HESS, false>(a, s);
+  switch (f3_kb(a.n)) {
+    CHF_CASE_KB(1) CHF_CASE_KB(2) CHF_CASE_KB(4) CHF_CASE_KB(8) CHF_CASE_KB(16)
+  }
+#undef CHF_CASE_KB
+  return cudaErrorInvalidValue;
+}
+
+template <bool HESS>
+int run(int func, int n, int csize, int64_t m, const double* points, const double* vecs, double* out,
+        const double* params, cudaStream_t s) {
+  BatchArgs a;
+  a.n = n;
+  a.csize = csize;
+  a.groups = 1;
+  a.m = m;
+  a.points = points;
+  a.vecs = vecs;
+  a.out = out;
+  a.params = params;
+  const cudaError_t e = (func == CHESSFAD_FLETCHER_POWELL) ? dispatch_f3<HESS>(a, s) : dispatch_reg<HESS>(func, csize, a, s);
+  return e == cudaSuccess ? CHESSFAD_OK : CHESSFAD_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------- FP64 probe kernel
+__global__ void __launch_bounds__(256) fp64_probe_kernel(int64_t iters, double* sink) {
+  const double b = 1.0 + 1e-16 * threadIdx.x, c = 1e-300;
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int64_t it = 0; it < iters; it++) {
+    x0 = fma(x0, b, c); x1 = fma(x1, b, c); x2 = fma(x2, b, c); x3 = fma(x3, b, c);
+    x4 = fma(x4, b, c); x5 = fma(x5, b, c); x6 = fma(x6, b, c); x7 = fma(x7, b, c);
+  }
+  sink[(size_t)blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+
+}  // namespace
+
+extern "C" {
+
+int chessfad_hvp_batch(int func, int n, int csize, int64_t m, const double* points, const double* vecs, double* out,
+                       const double* params, void* stream) {
+  int st = validate(func, n, csize, m, false, params, points, vecs, out);
+  if (st) return st;
+  if (!supported(func, n, csize)) return CHESSFAD_ERR_UNSUPPORTED;
+  if (m == 0) return CHESSFAD_OK;
+  return run<false>(func, n, csize, m, points, vecs, out, params, (cudaStream_t)stream);
+}
+
+int chessfad_hessian_batch(int func, int n, int csize, int64_t m, const double* points, double* hess,
+                           const double* params, void* stream) {
+  int st = validate(func, n, csize, m, false, params, points, hess, hess);
+  if (st) return st;
+  if (!supported(func, n, csize)) return CHESSFAD_ERR_UNSUPPORTED;
+  if (m == 0) return CHESSFAD_OK;
+  return run<true>(func, n, csize, m, points, nullptr, hess, params, (cudaStream_t)stream);
+}
+
+int chessfad_hvp_batch_host(int func, int n, int csize, int64_t m, const double* points, const double* vecs,
+                            double* out, const double* params, int64_t piece_points, void* stream) {
+  int st = validate(func, n, csize, m, false, params, points, vecs, out);
+  if (st) return st;
+  if (!supported(func, n, csize)) return CHESSFAD_ERR_UNSUPPORTED;
+  if (m == 0) return CHESSFAD_OK;
+  cudaStream_t s0 = (cudaStream_t)stream;
+  if (piece_points <= 0) piece_points = std::max<int64_t>(4096, (m + 7) / 8);
+  piece_points = std::min(piece_points, m);
+  const int npieces = (int)((m + piece_points - 1) / piece_points);
+  const size_t row = (size_t)n * sizeof(double);
+  const size_t pbytes = (size_t)piece_points * row;
+  const size_t nparams = (func == CHESSFAD_FLETCHER_POWELL) ? (size_t)2 * n * n + n : 0;
+
+  cudaStream_t ss[2] = {nullptr, nullptr};
+  cudaEvent_t ready = nullptr, done[2] = {nullptr, nullptr};
+  double* d_buf = nullptr;
+  cudaError_t e = cudaSuccess;
+  auto ok = [&](cudaError_t x) { if (e == cudaSuccess) e = x; return e == cudaSuccess; };
+  // two buffer sets (points, vecs, out) so piece p+1 copies while piece p computes
+  const size_t total = 2 * 3 * pbytes + nparams * sizeof(double);
+  if (ok(cudaStreamCreateWithFlags(&ss[0], cudaStreamNonBlocking)) &&
+      ok(cudaStreamCreateWithFlags(&ss[1], cudaStreamNonBlocking)) &&
+      ok(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming)) &&
+      ok(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming)) &&
+      ok(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming)) &&
+      ok(cudaMallocAsync((void**)&d_buf, total, s0))) {
+    double* d_params = d_buf + 6 * (pbytes / sizeof(double));
+    if (nparams) ok(cudaMemcpyAsync(d_params, params, nparams * sizeof(double), cudaMemcpyHostToDevice, s0));
+    ok(cudaEventRecord(ready, s0));
+    ok(cudaStreamWaitEvent(ss[0], ready, 0));
+    ok(cudaStreamWaitEvent(ss[1], ready, 0));
+    for (int p = 0; p < npieces && e == cudaSuccess; p++) {
+      const int b = p & 1;
+      cudaStream_t s = ss[b];
+      double* dp = d_buf + (size_t)(3 * b) * (pbytes / sizeof(double));
+      double* dv = dp + pbytes / sizeof(double);
+      double* dout = dv + pbytes / sizeof(double);
+      const int64_t e0 = (int64_t)p * piece_points;
+      const int64_t cnt = std::min(piece_points, m - e0);
+      const size_t bytes = (size_t)cnt * row;
+      // same-stream ordering protects buffer set b (its previous D2H precedes these copies)
+      ok(cudaMemcpyAsync(dp, points + e0 * n, bytes, cudaMemcpyHostToDevice, s));
+      ok(cudaMemcpyAsync(dv, vecs + e0 * n, bytes, cudaMemcpyHostToDevice, s));
+      if (e == cudaSuccess) {
+        const int r = run<false>(func, n, csize, cnt, dp, dv, dout, nparams ? d_params : nullptr, s);
+        if (r != CHESSFAD_OK) e = cudaErrorLaunchFailure;
+      }
+      ok(cudaMemcpyAsync(out + e0 * n, dout, bytes, cudaMemcpyDeviceToHost, s));
+    }
+    ok(cudaEventRecord(done[0], ss[0]));
+    ok(cudaEventRecord(done[1], ss[1]));
+    ok(cudaStreamWaitEvent(s0, done[0], 0));
+    ok(cudaStreamWaitEvent(s0, done[1], 0));
+    ok(cudaFreeAsync(d_buf, s0));
+    ok(cudaStreamSynchronize(s0));
+  }
+  for (int b = 0; b < 2; b++) {
+    if (ss[b]) cudaStreamDestroy(ss[b]);
+    if (done[b]) cudaEventDestroy(done[b]);
+  }
+  if (ready) cudaEventDestroy(ready);
+  return e == cudaSuccess ? CHESSFAD_OK : CHESSFAD_ERR_CUDA;
+}
+
+int chessfad_is_supported(int func, int n, int csize) {
+  if (validate(func, n, csize, 0, false, func == CHESSFAD_FLETCHER_POWELL ? (const void*)1 : nullptr, nullptr,
+               nullptr, nullptr))
+    return 0;
+  return supported(func, n, csize);
+}
+
+const char* chessfad_status_string(int status) {
+  switch (status) {
+    case CHESSFAD_OK: return "CHESSFAD_OK";
+    case CHESSFAD_ERR_ARG: return "CHESSFAD_ERR_ARG: n < 1, m < 0 or NULL data pointer";
+    case CHESSFAD_ERR_CHUNK: return "CHESSFAD_ERR_CHUNK: csize must satisfy 1 <= csize <= n and csize | n";
+    case CHESSFAD_ERR_FUNC: return "CHESSFAD_ERR_FUNC: unknown function, n < 2, or missing Fletcher-Powell params";
+    case CHESSFAD_ERR_UNSUPPORTED: return "CHESSFAD_ERR_UNSUPPORTED: (func, n, csize) not in the compiled set";
+    case CHESSFAD_ERR_CUDA: return "CHESSFAD_ERR_CUDA: CUDA runtime error";
+  }
+  return "CHESSFAD: unknown status";
+}
+
+double chessfad_model_flops_per_point(int func, int n, int csize, int hessian) {
+  if (validate(func, n, csize, 0, false, (const void*)1, nullptr, nullptr, nullptr)) return -1.0;
+  const double C = csize, N = n;
+  // per-evaluation hDual op counts of the canonical forms (DESIGN.md op table)
+  double hm = 0, ha = 0, sm = 0, sa = 0, un = 0;
+  switch (func) {
+    case CHESSFAD_ROSENBROCK: hm = 3 * (N - 1); ha = 3 * N - 4; sm = N - 1; sa = N - 1; break;
+    case CHESSFAD_ACKLEY: hm = N; ha = 2 * N - 1; sm = N + 4; sa = 1; un = N + 3; break;
+    case CHESSFAD_FLETCHER_POWELL: hm = N; ha = 2 * N * N - 1; sm = 2 * N * N; sa = N; un = 2 * N; break;
+    case CHESSFAD_PRODSUM: hm = N - 1; ha = N - 2; break;
+  }
+  const double per_eval = hm * (10 * C + 4) + ha * (2 * C + 2) + sm * (2 * C + 2) + sa + un * (4 * C + 2);
+  return (N * N / C) * per_eval + (hessian ? 0.0 : 2 * N * N);
+}
+
+int chessfad_fp64_probe(int blocks, int64_t iters, double* sink, void* stream) {
+  if (blocks < 1 || iters < 0 || !sink) return CHESSFAD_ERR_ARG;
+  fp64_probe_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(iters, sink);
+  return cudaGetLastError() == cudaSuccess ? CHESSFAD_OK : CHESSFAD_ERR_CUDA;
+}
+
+const char* chessfad_version(void) { return "chessfad-b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+// testfuncs.cuh -- the paper's test functions over hDual<C> (device code).
+//
+// The paper names Rosenbrock, Ackley and Fletcher-Powell without formulas;
+// the definitions are SPEC.md:352-396 and the expression forms are DESIGN.md's canonical
+// forms (loops ascend, first term of every sum initialises).  The GPU may differ from the
+// oracle only in FMA contraction and in the order of reductions.
+//
+// Bodies are generic over a seed provider `y(k)` that returns the CHUNK-INIT seed of
+// variable k (Alg 4) on the fly: the paper's per-thread array
+// hDual<C> y[n] is never materialised.
+//
+// Fletcher-Powell is in f3.cuh (its O(n^2) hDual sums need a different schedule).
+#pragma once
+#include "hdual.cuh"
+
+namespace chessfad {
+
+enum { FUNC_ROSENBROCK = 0, FUNC_ACKLEY = 1, FUNC_FLETCHER_POWELL = 2, FUNC_PRODSUM = 3 };
+
+// CHUNK-INIT seed for the lane's own point; row i and chunk start cs are warp-uniform.
+//   y[k] = < a_k, [k==i], e_{k-cs} if cs <= k < cs+C, 0 ... 0 >          (Alg 4)
+template <int C>
+struct LaneSeed {
+  const double* a;  // a[k * stride] = coordinate k of this lane's point (shared memory)
+  int stride;
+  int i, cs;
+  CHF_INL hd<C> operator()(int k) const {
+    hd<C> y;
+    y.v[0] = a[k * stride];
+    y.v[1] = (k == i) ? 1.0 : 0.0;
+    const int off = k - cs;
+#pragma unroll
+    for (int l = 0; l < C; l++) y.v[2 + l] = (off == l) ? 1.0 : 0.0;
+#pragma unroll
+    for (int l = 0; l < C; l++) y.v[C + 2 + l] = 0.0;
+    return y;
+  }
+};
+
+// F1 Rosenbrock: s = sum_{i<n-1} 100 (y_{i+1} - y_i^2)^2 + (1 - y_i)^2
+// per evaluation: 3(n-1) hh*, 3n-4 hh+, n-1 s*, n-1 s+  (DESIGN.md op table)
+template <int C, class Seed>
+CHF_INL hd<C> f_rosenbrock(int n, const Seed& y) {
+  hd<C> s;
+  {
+    const hd<C> y0 = y(0), y1 = y(1);
+    const hd<C> d = y1 - y0 * y0;
+    const hd<C> e = 1.0 - y0;
+    s = 100.0 * (d * d) + e * e;
+  }
+#pragma unroll 2
+  for (int i = 1; i < n - 1; i++) {
+    const hd<C> yi = y(i), yi1 = y(i + 1);
+    const hd<C> d = yi1 - yi * yi;
+    const hd<C> e = 1.0 - yi;
+    const hd<C> t = 100.0 * (d * d) + e * e;
+    s = s + t;
+  }
+  return s;
+}
+
+// F2 Ackley: -20 exp(-0.2 sqrt(S1/n)) - exp(S2/n) + 20 + e,  S1 = sum y^2, S2 = sum cos(2 pi y)
+// (SPEC.md:361-369); per evaluation n hh*, 2n-1 hh+, n+4 s*, n+3 unary, 1 s+
+template <int C, class Seed>
+CHF_INL hd<C> f_ackley(int n, const Seed& y) {
+  const double two_pi = 6.283185307179586, euler = 2.718281828459045;
+  hd<C> s1;
+  {
+    const hd<C> y0 = y(0);
+    s1 = y0 * y0;
+  }
+  for (int i = 1; i < n; i++) {
+    const hd<C> yi = y(i);
+    s1 = s1 + yi * yi;
+  }
+  hd<C> s2 = cos(two_pi * y(0));
+  for (int i = 1; i < n; i++) s2 = s2 + cos(two_pi * y(i));
+  const double inv_n = 1.0 / n;
+  const hd<C> t1 = (-20.0) * exp((-0.2) * sqrt(s1 * inv_n));
+  const hd<C> t2 = exp(s2 * inv_n);
+  return (t1 - t2) + (20.0 + euler);
+}
+
+// F4 prodsum: sum_{i<n-1} y_i y_{i+1}; exactly n-1 hh* and n-2 hh+ 
+template <int C, class Seed>
+CHF_INL hd<C> f_prodsum(int n, const Seed& y) {
+  hd<C> s = y(0) * y(1);
+#pragma unroll 2
+  for (int i = 1; i < n - 1; i++) s = s + y(i) * y(i + 1);
+  return s;
+}
+
+template <int FUNC, int C, class Seed>
+CHF_INL hd<C> eval_f(int n, const Seed& y) {
+  if constexpr (FUNC == FUNC_ROSENBROCK) return f_rosenbrock<C>(n, y);
+  else if constexpr (FUNC == FUNC_ACKLEY) return f_ackley<C>(n, y);
+  else return f_prodsum<C>(n, y);
+}
+
+}  // namespace chessfad

@@ -1,0 +1,112 @@
+"""The C-ABI library loads and exports every symbol include/chessfad.h declares; argument
+validation and the model-FLOP count work without a GPU (no compute call is made)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import paper_2410_22575_b200 as chf
+    return chf.load()
+
+
+def declared_symbols():
+    hdr = open(os.path.join(ROOT, "include", "chessfad.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    return sorted(set(re.findall(r"\b(chessfad_\w+)\s*\(", hdr)))
+
+
+def test_exports_every_declared_symbol(lib):
+    import paper_2410_22575_b200 as chf
+    syms = declared_symbols()
+    assert len(syms) >= 8
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert sorted(chf.EXPORTS) == syms
+
+
+def test_sm100a_cubin_embedded():
+    """The library carries sm_100a SASS (cuobjdump lists the ELF arch)."""
+    import shutil
+    import subprocess
+    import paper_2410_22575_b200 as chf
+    chf.load()
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([exe, "--list-elf", chf.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_status_and_version(lib):
+    import paper_2410_22575_b200 as chf
+    assert "sm_100a" in chf.version()
+    for st in range(6):
+        assert lib.chessfad_status_string(st).decode().startswith("CHESSFAD")
+
+
+def _call(lib, func, n, C, m, pts=1, vec=1, out=1, params=None):
+    vp = lambda x: None if x is None else ctypes.c_void_p(x)
+    return lib.chessfad_hvp_batch(func, n, C, m, vp(pts), vp(vec), vp(out), vp(params), None)
+
+
+def test_argument_errors(lib):
+    assert _call(lib, 0, 0, 1, 10) == 1          # n < 1
+    assert _call(lib, 0, 4, 1, -1) == 1          # m < 0
+    assert _call(lib, 0, 4, 1, 10, pts=None) == 1  # NULL with m > 0
+    assert _call(lib, 0, 4, 3, 10) == 2          # C does not divide n
+    assert _call(lib, 0, 4, 0, 10) == 2          # C < 1
+    assert _call(lib, 0, 4, 8, 10) == 2          # C > n
+    assert _call(lib, 0, 1, 1, 10) == 3          # Rosenbrock n < 2
+    assert _call(lib, 3, 1, 1, 10) == 3          # prodsum n < 2
+    assert _call(lib, 9, 4, 1, 10) == 3          # unknown func
+    assert _call(lib, 2, 4, 1, 10, params=None) == 3  # F3 without params
+    assert _call(lib, 0, 12, 3, 10) == 4         # C=3 not compiled for the register path
+    assert _call(lib, 0, 4, 1, 0, None, None, None) == 0  # m == 0: empty no-op, no CUDA call
+    assert lib.chessfad_hessian_batch(0, 4, 3, 10, ctypes.c_void_p(1), ctypes.c_void_p(1), None, None) == 2
+
+
+def test_is_supported(lib):
+    import paper_2410_22575_b200 as chf
+    assert chf.is_supported("rosenbrock", 16, 4)
+    assert not chf.is_supported("rosenbrock", 16, 3)
+    assert not chf.is_supported("rosenbrock", 12, 3)
+    assert chf.is_supported("fletcher_powell", 12, 3)  # runtime-C schedule
+    assert chf.is_supported("fletcher_powell", 128, 8)
+    assert not chf.is_supported("fletcher_powell", 256, 8)
+
+
+FUNCS = ["rosenbrock", "ackley", "fletcher_powell", "prodsum"]
+
+
+@pytest.mark.parametrize("func", FUNCS)
+@pytest.mark.parametrize("n,C", [(2, 1), (4, 2), (8, 4), (6, 6)])
+def test_model_flops_match_oracle_counts(func, n, C):
+    """chessfad_model_flops_per_point (library) == scalar mul+add counted by the oracle's
+    counting build running Alg 7 (independent code, same Fig. 1 / §V accounting)."""
+    import paper_2410_22575_b200 as chf
+    params = synth.fp_params_flat(0, n) if func == "fletcher_powell" else None
+    a = synth.points(0, n, 1)[0] + 3.0
+    _, c = oracle.count(oracle.chess_vec, func, a, a, C, params)
+    assert chf.model_flops_per_point(func, n, C) == c["mul"] + c["add"]
+    _, c = oracle.count(oracle.hessian, func, a, params, algo="chunk", C=C)
+    assert chf.model_flops_per_point(func, n, C, hessian=True) == c["mul"] + c["add"]
+
+
+def test_model_flops_survey_table():
+    """Spot values of SURVEY §8(d)'s model-FLOP table."""
+    import paper_2410_22575_b200 as chf
+    assert chf.model_flops_per_point("rosenbrock", 2, 1) == 228
+    assert chf.model_flops_per_point("rosenbrock", 16, 1) == 226048
+    assert chf.model_flops_per_point("rosenbrock", 16, 16) == 150928
+    assert chf.model_flops_per_point("ackley", 16, 4) == 100160
+    assert chf.model_flops_per_point("fletcher_powell", 16, 2) == pytest.approx(878e3, rel=1e-3)

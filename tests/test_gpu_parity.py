@@ -1,0 +1,215 @@
+"""CUDA path vs the CPU oracle, element by element, through the C-ABI (libchessfad.so).
+
+Metric: componentwise err_{e,i} = |g - r| / max(|r|, s_{e,i}),
+s = sum_j |H_ij||v_j| from the oracle; the north-star bar is max err <= 1e-10.  The
+expected margin is ~1e-15 (FMA contraction + reduction order only), so every test also
+asserts a tighter 1e-12 that a real bug (wrong slot / seed / term) cannot pass.
+Integer-valued inputs must match the exact closed form bit for bit.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests import closed_forms as cf
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+FUNCS = ["rosenbrock", "ackley", "fletcher_powell", "prodsum"]
+TOL = 1e-10
+TIGHT = 1e-12
+
+
+@pytest.fixture(scope="module")
+def chf():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2410_22575_b200 as m
+    m.load()
+    return m
+
+
+def _params(func, n, seed=0):
+    return synth.fp_params_flat(seed, n) if func == "fletcher_powell" else None
+
+
+def _gpu_hvp(chf, func, P, V, C, params=None):
+    dev = torch.device("cuda")
+    p = torch.from_numpy(P).to(dev)
+    v = torch.from_numpy(V).to(dev)
+    pr = None if params is None else torch.from_numpy(params).to(dev)
+    out = chf.hvp_batch(func, p, v, C, pr)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def _check(gpu, ref, sabs, tol=TOL):
+    err = oracle.componentwise_error(gpu, ref, sabs)
+    assert np.all(np.isfinite(gpu))
+    assert err.max() <= tol, f"max componentwise err {err.max():.3e}"
+    assert err.max() <= TIGHT, f"max componentwise err {err.max():.3e} (tight bar)"
+    return float(err.max())
+
+
+def divisors(n):
+    return [c for c in range(1, n + 1) if n % c == 0]
+
+
+# ------------------------------------------------------------ config 1: n=2, C=1, m=1024, every point
+def test_config1_every_point(chf):
+    n, m = 2, 1024
+    P, V = synth.points(0, n, m), synth.vectors(0, n, m)
+    for func in FUNCS:
+        params = _params(func, n)
+        ref, sabs = oracle.hvp_batch(func, P, V, 1, params)
+        _check(_gpu_hvp(chf, func, P, V, 1, params), ref, sabs)
+
+
+# ------------------------------------------------------------ sweep of n, C: several tiles + ragged tail
+@pytest.mark.parametrize("func", FUNCS)
+@pytest.mark.parametrize("n", [2, 3, 4, 8, 16, 32])
+def test_parity_sweep(chf, func, n):
+    m = 3 * 32 * 8 + 13  # several CTAs of the widest tile and a ragged tail
+    if func == "fletcher_powell" and n >= 32:
+        m = 301
+    P, V = synth.points(1, n, m), synth.vectors(1, n, m)
+    params = _params(func, n)
+    ref, sabs = oracle.hvp_batch(func, P, V, 1, params)  # the oracle is C-invariant
+    for C in divisors(n):
+        if not chf.is_supported(func, n, C):
+            continue
+        _check(_gpu_hvp(chf, func, P, V, C, params), ref, sabs)
+
+
+@pytest.mark.parametrize("func", FUNCS)
+def test_large_n(chf, func):
+    for n in (64, 128):
+        m = (45 if n == 64 else 9) if func == "fletcher_powell" else 70
+        P, V = synth.points(2, n, m), synth.vectors(2, n, m)
+        params = _params(func, n)
+        ref, sabs = oracle.hvp_batch(func, P, V, n if n <= 32 else 32, params)
+        for C in [1, 8, 32]:
+            if chf.is_supported(func, n, C):
+                _check(_gpu_hvp(chf, func, P, V, C, params), ref, sabs)
+
+
+# ------------------------------------------------------------ bit-exact integer pin
+@pytest.mark.parametrize("func", ["rosenbrock", "prodsum"])
+@pytest.mark.parametrize("n", [2, 4, 8, 16])
+def test_integer_inputs_bitwise(chf, func, n):
+    """Integer points/vectors in {-9..9}: every intermediate is an exact integer, so the GPU
+    must equal the exact rational closed form bit for bit under any FMA/reduction order."""
+    m = 300
+    P, V = synth.int_points(5, n, m), synth.int_vectors(5, n, m)
+    want = np.zeros((m, n))
+    for e in range(m):
+        H = cf.rosenbrock_hessian_exact(P[e]) if func == "rosenbrock" else cf.prodsum_hessian_exact(n)
+        want[e] = [float(x) for x in cf.exact_hvp(H, V[e])]
+    for C in divisors(n):
+        if chf.is_supported(func, n, C):
+            assert np.array_equal(_gpu_hvp(chf, func, P, V, C), want)
+
+
+def test_golden_values(chf):
+    got = _gpu_hvp(chf, "rosenbrock", np.array([[1.0, 2, 3, 4]]), np.ones((1, 4)), 2)
+    assert np.array_equal(got[0], [2.0, 2602.0, 7402.0, -1000.0])
+    got = _gpu_hvp(chf, "rosenbrock", np.array([[1.0, 1.0]]), np.ones((1, 2)), 1)
+    assert np.array_equal(got[0], [402.0, -200.0])
+    got = _gpu_hvp(chf, "ackley", np.array([[0.5, -0.25]]), np.array([[1.0, 2.0]]), 2)
+    np.testing.assert_allclose(got[0], [-7.2973882525010968, -2.6223411680113156], rtol=1e-14)
+
+
+# ------------------------------------------------------------ Hessian API (Alg 5)
+@pytest.mark.parametrize("func", FUNCS)
+def test_hessian_parity(chf, func):
+    n, m = 32, 200
+    P = synth.points(3, n, m)
+    params = _params(func, n)
+    ref = oracle.hessian_batch(func, P, 4, params)
+    dev = torch.device("cuda")
+    pr = None if params is None else torch.from_numpy(params).to(dev)
+    for C in divisors(n):
+        if not chf.is_supported(func, n, C):
+            continue
+        H = chf.hessian_batch(func, torch.from_numpy(P).to(dev), C, pr).cpu().numpy()
+        scale = np.abs(ref).reshape(m, -1).max(axis=1)
+        err = (np.abs(H - ref).reshape(m, -1).max(axis=1) / scale).max()
+        assert err <= TIGHT, (C, err)
+        sym = (np.abs(H - H.transpose(0, 2, 1)).reshape(m, -1).max(axis=1) / scale).max()
+        assert sym <= 1e-13
+
+
+def test_hessian_closed_form_rosenbrock(chf):
+    n, m = 32, 64
+    P = synth.int_points(9, n, m)
+    H = chf.hessian_batch("rosenbrock", torch.from_numpy(P).cuda(), 8).cpu().numpy()
+    for e in range(m):
+        assert np.array_equal(H[e], cf.to_float(cf.rosenbrock_hessian_exact(P[e])))
+
+
+# ------------------------------------------------------------ edge cases
+def test_edge_cases(chf):
+    dev = torch.device("cuda")
+    # m == 0
+    out = chf.hvp_batch("rosenbrock", torch.empty((0, 4), dtype=torch.float64, device=dev),
+                        torch.empty((0, 4), dtype=torch.float64, device=dev), 2)
+    assert out.shape == (0, 4)
+    # m == 1 and m == 33 (one full group + 1)
+    for m in (1, 33):
+        P, V = synth.points(4, 16, m), synth.vectors(4, 16, m)
+        ref, sabs = oracle.hvp_batch("ackley", P, V, 4)
+        _check(_gpu_hvp(chf, "ackley", P, V, 16, None), ref, sabs)
+    # Ackley at the origin: NaN derivatives propagate (not an error)
+    got = _gpu_hvp(chf, "ackley", np.zeros((2, 4)), np.ones((2, 4)), 2)
+    assert np.all(np.isnan(got))
+    # Ackley n = 1
+    P, V = synth.points(6, 1, 50), synth.vectors(6, 1, 50)
+    ref, sabs = oracle.hvp_batch("ackley", P, V, 1)
+    _check(_gpu_hvp(chf, "ackley", P, V, 1), ref, sabs)
+    # errors surface as exceptions
+    with pytest.raises(chf.ChessfadError, match="ERR_CHUNK"):
+        _gpu_hvp(chf, "rosenbrock", np.zeros((4, 6)), np.zeros((4, 6)), 4)
+    with pytest.raises(TypeError):
+        chf.hvp_batch("rosenbrock", torch.zeros((4, 4), dtype=torch.float32, device=dev),
+                      torch.zeros((4, 4), dtype=torch.float32, device=dev), 2)
+
+
+def test_determinism_and_shards(chf):
+    """No atomics, fixed order: bitwise identical run to run, and a batch computed in
+    shards (as the multi-GPU driver does) equals the unsharded batch bit for bit."""
+    n, m = 16, 4096 + 7
+    P, V = synth.points(8, n, m), synth.vectors(8, n, m)
+    for func in FUNCS:
+        params = _params(func, n)
+        a = _gpu_hvp(chf, func, P, V, 4, params)
+        b = _gpu_hvp(chf, func, P, V, 4, params)
+        assert np.array_equal(a, b)
+        cuts = [0, 1000, 1001, 2500, m]
+        parts = [_gpu_hvp(chf, func, P[c0:c1], V[c0:c1], 4, params) for c0, c1 in zip(cuts[:-1], cuts[1:])]
+        assert np.array_equal(np.concatenate(parts), a)
+
+
+def test_host_api_matches_device_api(chf):
+    n, m = 16, 5000
+    P, V = synth.points(10, n, m), synth.vectors(10, n, m)
+    for func in FUNCS:
+        params = _params(func, n)
+        dev_out = _gpu_hvp(chf, func, P, V, 8, params)
+        host_out = chf.hvp_batch_host(func, P, V, 8, params, piece_points=999)
+        assert np.array_equal(np.asarray(host_out), dev_out)
+
+
+# ------------------------------------------------------------ full size, bench launch configuration
+@pytest.mark.parametrize("func", FUNCS)
+def test_full_size_sampled(chf, func):
+    """cfg2 at BASELINE size (n=16, m=2^20) in the bench launch configuration; the oracle
+    checks a deterministic sample (first, last, fixed stride) point by point."""
+    n, m = 16, 1 << 20
+    P, V = synth.points(0, n, m), synth.vectors(0, n, m)
+    params = _params(func, n)
+    idx = np.unique(np.concatenate([[0, m - 1], np.arange(0, m, 4099)]))
+    ref, sabs = oracle.hvp_batch(func, P[idx], V[idx], 16, params)
+    for C in (1, 4, 16):
+        got = _gpu_hvp(chf, func, P, V, C, params)
+        _check(got[idx], ref, sabs)
