@@ -5,15 +5,26 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../include/chessfad.h"
 #include "launch.cuh"
 
 using namespace chessfad;
 
+namespace chessfad {
+int reg_warps() {
+  static const int w = [] {
+    const char* e = getenv("CHESSFAD_REG_WARPS");
+    return (e && atoi(e) == 8) ? 8 : 4;
+  }();
+  return w;
+}
+}  // namespace chessfad
+
 namespace {
 
-constexpr int kMaxNReg = 256;  // register-hDual path: 3*n*33*8 B of shared memory per CTA
+constexpr int kMaxNReg = 256;  // register-hDual path: (3 or 5)*n*33*8 B of shared memory per CTA
 constexpr int kMaxNF3 = 128;   // F3 path: per-thread R0/R1 scratch of 128 doubles
 
 bool reg_chunk_compiled(int C) { return C == 1 || C == 2 || C == 4 || C == 8 || C == 16 || C == 32; }
@@ -41,7 +52,9 @@ int validate(int func, int n, int csize, int64_t m, bool need_params_ptr, const 
 
 int supported(int func, int n, int csize) {
   if (func == CHESSFAD_FLETCHER_POWELL) return n <= kMaxNF3;
-  return n <= kMaxNReg && reg_chunk_compiled(csize);
+  const int fn = func == CHESSFAD_ACKLEY ? FUNC_ACKLEY : FUNC_ROSENBROCK;
+  const size_t smem = std::max(reg_smem_bytes(fn, n, groups_for(n, 4), false), reg_smem_bytes(fn, n, groups_for(n, 8), false));
+  return n <= kMaxNReg && smem <= 227 * 1024 && reg_chunk_compiled(csize);
 }
 
 // largest power of two <= 16 that divides n: the F3 k-block

@@ -31,7 +31,6 @@ struct BatchArgs {
 };
 
 constexpr int kPad = 33;          // shared-memory row stride (doubles) of [k][lane] tiles
-constexpr int kWarpsGeneric = 8;  // register-hDual path: 256 threads per CTA
 constexpr int kWarpsF3 = 4;       // Fletcher-Powell path: 128 threads per CTA
 
 // stage points [and vectors] of the tile into shared memory, transposed per 32-point group
@@ -57,28 +56,39 @@ CHF_INL void write_tile(const BatchArgs& p, int64_t e0, int P, const double* s_o
 }
 
 // ---------------------------------------------------------------- F1, F2, F4: hDual<C> in registers
-template <int FUNC, int C, bool HESS>
-__global__ void __launch_bounds__(kWarpsGeneric * 32) hvp_reg_kernel(BatchArgs p) {
+template <int FUNC, int C, bool HESS, int W>
+__global__ void __launch_bounds__(W * 32) hvp_reg_kernel(BatchArgs p) {
   extern __shared__ double smem[];
   const int n = p.n, G = p.groups, P = 32 * G;
   double* s_pts = smem;
   double* s_vec = HESS ? nullptr : s_pts + G * n * kPad;
   double* s_out = HESS ? nullptr : s_vec + G * n * kPad;
+  double* s_sin = (HESS ? s_pts : s_out) + G * n * kPad;  // Ackley only
+  double* s_cos = s_sin + G * n * kPad;
   const int64_t e0 = (int64_t)blockIdx.x * P;
   stage_tile(p, e0, P, s_pts, s_vec);
+  if (FUNC == FUNC_ACKLEY) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < G * n * 32; q += blockDim.x) {
+      const int idx = (q >> 5) * kPad + (q & 31);
+      sincos(6.283185307179586 * s_pts[idx], s_sin + idx, s_cos + idx);
+    }
+  }
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = warp % G, rstep = kWarpsGeneric / G;
+  const int g = warp % G, rstep = W / G;
   const double* a = s_pts + g * n * kPad + lane;
   const double* v = HESS ? nullptr : s_vec + g * n * kPad + lane;
+  const double* tsin = FUNC == FUNC_ACKLEY ? s_sin + g * n * kPad + lane : nullptr;
+  const double* tcos = FUNC == FUNC_ACKLEY ? s_cos + g * n * kPad + lane : nullptr;
   const int64_t e = e0 + g * 32 + lane;
   const int nchunk = n / C;
   for (int i = warp / G; i < n; i += rstep) {
     double res = 0.0;
     for (int j = 0; j < nchunk; j++) {
       const int cs = j * C;
-      const LaneSeed<C> y{a, kPad, i, cs};
+      const LaneSeed<C> y{a, kPad, i, cs, tsin, tcos};
       const hd<C> t = eval_f<FUNC, C>(n, y);  // CHUNK-INIT + f<hDual<C>>, Alg 7 :389-390
       if (HESS) {
         if (e < p.m) {

@@ -14,7 +14,9 @@ inline int groups_for(int n, int warps) {
   return g;
 }
 
-inline size_t reg_smem_bytes(int n, int G, bool hess) { return (size_t)(hess ? 1 : 3) * G * n * kPad * sizeof(double); }
+inline size_t reg_smem_bytes(int func, int n, int G, bool hess) {
+  return (size_t)((hess ? 1 : 3) + (func == FUNC_ACKLEY ? 2 : 0)) * G * n * kPad * sizeof(double);
+}
 
 inline size_t f3_smem_bytes(int n, int G, bool hess, bool ab_smem) {
   return (size_t)(hess ? 2 : 4) * G * n * kPad * sizeof(double) + (ab_smem ? (size_t)n * n * 2 * sizeof(double) : 0);
@@ -30,13 +32,21 @@ inline cudaError_t launch_with_smem(K kernel, int grid, int block, size_t smem, 
   return cudaGetLastError();
 }
 
-template <int FUNC, int C, bool HESS>
-cudaError_t launch_reg(BatchArgs a, cudaStream_t s) {
-  a.groups = groups_for(a.n, kWarpsGeneric);
+// warps per CTA of the register path (tuning knob CHESSFAD_REG_WARPS = 4 | 8, read once)
+int reg_warps();
+
+template <int FUNC, int C, bool HESS, int W>
+cudaError_t launch_reg_w(BatchArgs a, cudaStream_t s) {
+  a.groups = groups_for(a.n, W);
   const int64_t P = 32 * a.groups;
   const int grid = (int)((a.m + P - 1) / P);
-  return launch_with_smem(hvp_reg_kernel<FUNC, C, HESS>, grid, kWarpsGeneric * 32,
-                          reg_smem_bytes(a.n, a.groups, HESS), s, a);
+  return launch_with_smem(hvp_reg_kernel<FUNC, C, HESS, W>, grid, W * 32, reg_smem_bytes(FUNC, a.n, a.groups, HESS),
+                          s, a);
+}
+
+template <int FUNC, int C, bool HESS>
+cudaError_t launch_reg(BatchArgs a, cudaStream_t s) {
+  return reg_warps() == 8 ? launch_reg_w<FUNC, C, HESS, 8>(a, s) : launch_reg_w<FUNC, C, HESS, 4>(a, s);
 }
 
 template <int KB, bool HESS, bool AB_SMEM>

@@ -24,6 +24,10 @@ struct LaneSeed {
   const double* a;  // a[k * stride] = coordinate k of this lane's point (shared memory)
   int stride;
   int i, cs;
+  // Ackley: sin/cos of the value slot 2*pi*a_k of cos(2*pi*y_k), tabulated once per tile
+  // (g, g', g'' of an input-only argument; the model counts them as 0 FLOPs)
+  const double* sin2pi;
+  const double* cos2pi;
   CHF_INL hd<C> operator()(int k) const {
     hd<C> y;
     y.v[0] = a[k * stride];
@@ -73,8 +77,15 @@ CHF_INL hd<C> f_ackley(int n, const Seed& y) {
     const hd<C> yi = y(i);
     s1 = s1 + yi * yi;
   }
-  hd<C> s2 = cos(two_pi * y(0));
-  for (int i = 1; i < n; i++) s2 = s2 + cos(two_pi * y(i));
+  // cos(u), u = 2 pi y_i: (g, g', g'') = (cos u0, -sin u0, -cos u0) with u0 = 2 pi a_i,
+  // bit-identical to the tabulated argument (same single rounding of two_pi * a_i)
+  auto cos2pi = [&](int k) {
+    const hd<C> u = two_pi * y(k);
+    const double s = y.sin2pi[k * y.stride], c = y.cos2pi[k * y.stride];
+    return hd_unary(u, c, -s, -c);
+  };
+  hd<C> s2 = cos2pi(0);
+  for (int i = 1; i < n; i++) s2 = s2 + cos2pi(i);
   const double inv_n = 1.0 / n;
   const hd<C> t1 = (-20.0) * exp((-0.2) * sqrt(s1 * inv_n));
   const hd<C> t2 = exp(s2 * inv_n);

@@ -1,0 +1,51 @@
+"""Summarise an ncu --csv metric log of tools/profile_sweep.py: executed FP64 FLOPs
+(2*DFMA + DMUL + DADD) vs model FLOPs, FP64 pipe utilisation, DRAM traffic."""
+import csv
+import json
+import re
+import sys
+
+
+def load(csv_path, order_path):
+    order = [l.split() for l in open(order_path) if l.startswith("launch ")]
+    rows = list(csv.reader(l for l in open(csv_path) if not l.startswith("==")))
+    hdr = rows[0]
+    ix = {h: i for i, h in enumerate(hdr)}
+    per = {}
+    for r in rows[1:]:
+        if len(r) < len(hdr):
+            continue
+        lid = int(r[ix["ID"]])
+        per.setdefault(lid, {})[r[ix["Metric Name"]]] = float(r[ix["Metric Value"]].replace(",", ""))
+    out = []
+    for lid, (k, v) in enumerate(sorted(per.items())):
+        if lid >= len(order):
+            break
+        _, func, n, C, m, fl = order[lid]
+        n, C, m = int(n[2:]), int(C[2:]), int(m[2:])
+        model = float(fl.split("=")[1]) * m
+        ex = 2 * v["sm__sass_thread_inst_executed_op_dfma_pred_on.sum"] + v["sm__sass_thread_inst_executed_op_dmul_pred_on.sum"] + v["sm__sass_thread_inst_executed_op_dadd_pred_on.sum"]
+        t = v["gpu__time_duration.sum"] * 1e-9
+        out.append({"func": func, "n": n, "C": C, "m": m, "time_ms": t * 1e3,
+                    "model_flops": model, "executed_flops": ex, "executed_over_model": ex / model,
+                    "fp64_warp_inst": v["sm__inst_executed_pipe_fp64.sum"],
+                    "fp64_pipe_active_pct": v["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"],
+                    "executed_flop_per_fp64_lane_inst": ex / (32 * v["sm__inst_executed_pipe_fp64.sum"]),
+                    "all_warp_inst": v["smsp__inst_executed.sum"],
+                    "fp64_inst_share": v["sm__inst_executed_pipe_fp64.sum"] / v["smsp__inst_executed.sum"],
+                    "dram_bytes": v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"],
+                    "regs": v["launch__registers_per_thread"],
+                    "warps_active_pct": v["sm__warps_active.avg.pct_of_peak_sustained_active"],
+                    "sm_clock_ghz": v["sm__cycles_elapsed.avg.per_second"] / 1e9})
+    return out
+
+
+if __name__ == "__main__":
+    res = load(sys.argv[1], sys.argv[2])
+    print(f"{'func':16s} {'C':>3s} {'ms':>7s} {'exec/model':>10s} {'fp64pipe%':>9s} {'fl/inst':>7s} {'fp64share':>9s} {'DRAM MB':>8s} {'regs':>4s} {'warps%':>6s} {'GHz':>5s}")
+    for r in res:
+        print(f"{r['func']:16s} {r['C']:3d} {r['time_ms']:7.2f} {r['executed_over_model']:10.3f} {r['fp64_pipe_active_pct']:9.1f} "
+              f"{r['executed_flop_per_fp64_lane_inst']:7.3f} {r['fp64_inst_share']:9.3f} {r['dram_bytes']/1e6:8.1f} {r['regs']:4.0f} "
+              f"{r['warps_active_pct']:6.1f} {r['sm_clock_ghz']:5.2f}")
+    if len(sys.argv) > 3:
+        json.dump(res, open(sys.argv[3], "w"), indent=1)
