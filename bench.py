@@ -285,6 +285,8 @@ def main():
         "ms_per_step": e2e_t * 1e3, "api": "chessfad_hvp_batch_host (2-stream H2D/kernel/D2H pipeline)"}
 
     # ---- chunk sweep over the four functions (cfg2)
+    from paper_2410_22575_b200.build import source_hash
+    src_hash = source_hash()
     sweep = []
     if not args.no_sweep:
         for f in FUNCS:
@@ -294,9 +296,12 @@ def main():
                 ks = 10
                 tt = timed(f, c, ks, 3) / ks
                 fl = chf.model_flops_per_point(f, n, c)
+                exs = executed_entry(f, n, c, src_hash)
                 sweep.append({"func": f, "csize": c, "hvp_per_s": world * m / tt, "ms": tt * 1e3,
-                              "model_tflops_per_gpu": m * fl / tt / 1e12,
-                              "frac_fp64_nominal": m * fl / tt / 1e12 / peak_tf})
+                              "model_tflops_effective": m * fl / tt / 1e12,
+                              "executed_tflops": None if exs is None else m * exs["executed_flops_per_point"] / tt / 1e12,
+                              "executed_frac": None if exs is None else
+                              m * exs["executed_flops_per_point"] / tt / 1e12 / peak_tf})
 
     # ---- CPU baseline: the oracle on the host cores, rank 0 at N=1 only
     cpu = None
@@ -308,29 +313,36 @@ def main():
                "sample": f"{ms} points (first {ms} of the seeded cfg2 stream), {dt:.1f} s of Alg 7 in the plain C "
                          f"oracle, {threads} pthreads"}
 
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
-        try:
-            tr = json.load(open(prof))
-            key = f"{args.func}_n{n}_C{C}_m{m}"
-            traffic = tr.get(key)
-        except Exception:
-            traffic = None
+    # executed FP64 FLOPs of this build, measured by ncu (profiles/executed_flops.json)
+    from paper_2410_22575_b200.build import source_hash
+    ex = executed_entry(args.func, n, C, source_hash())
+    model_tf = achieved_tf
+    if ex is not None:
+        exec_tf = m * ex["executed_flops_per_point"] / per_step / 1e12
+        traffic = ex["dram_bytes_per_launch"] * m / ex["m"]
+        accounting = ("executed FP64 FLOPs (2*DFMA+DMUL+DADD per point, ncu, this build) x m / event time; "
+                      "model FLOPs reported as model_tflops_effective")
+    else:
+        exec_tf, traffic = None, None
+        accounting = "executed-FLOP table missing or stale for this build: achieved = model FLOPs (effective)"
+    achieved = exec_tf if exec_tf is not None else model_tf
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_config(args, world),
-            "roofline": {"bound": "alu", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved_tf / peak_tf, "traffic": traffic,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tf, "traffic": traffic, "accounting": accounting,
+                         "model_tflops_effective": model_tf, "model_frac_effective": model_tf / peak_tf,
+                         "executed_flops_per_point": None if ex is None else ex["executed_flops_per_point"],
+                         "fp64_pipe_active_pct_ncu": None if ex is None else ex["fp64_pipe_active_pct"],
                          "kernel": f"hvp_reg_kernel<{args.func},C={C}>" if args.func != "fletcher_powell"
                          else "hvp_f3_kernel",
                          "peak_basis": f"derived: {SMS} SMs x {FP64_FMA_PER_SM_CLK} FP64 FMA/clk x 2 x {peak_mhz:.0f} MHz "
                                        "(sm_max_mhz, MEASURED_PEAKS.json); DESIGN.md",
-                         "flops_basis": f"model FLOPs/point {flops_pt:.0f} (paper §V count, Fig. 1 per-op costs)",
-                         "fp64_probe_tflops": probe_tf, "frac_of_probe": achieved_tf / probe_tf},
+                         "model_flops_per_point": flops_pt,
+                         "fp64_probe_tflops": probe_tf, "frac_of_probe": achieved / probe_tf},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps, "clocks": clocks, "parity": parity,
             "sweep": sweep,
         }
@@ -338,6 +350,16 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def executed_entry(func, n, C, src_hash):
+    try:
+        tab = json.load(open(os.path.join(ROOT, "profiles", "executed_flops.json")))
+    except Exception:
+        return None
+    if tab.get("src_hash") != src_hash:
+        return None
+    return tab.get("entries", {}).get(f"{func} n={n} C={C}")
 
 
 class _Null:

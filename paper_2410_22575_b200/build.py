@@ -30,6 +30,18 @@ def _nvcc():
     return "nvcc"
 
 
+def source_hash() -> str:
+    """sha256 over the CUDA sources, the header and the compile flags: identifies the SASS
+    that the ncu-measured executed-FLOP table (profiles/executed_flops.json) describes."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in sorted(glob.glob(os.path.join(CSRC, "*.cu*"))) + [os.path.join(ROOT, "include", "chessfad.h")]:
+        h.update(os.path.basename(f).encode())
+        h.update(open(f, "rb").read())
+    h.update(" ".join(ARCH + NVCC_FLAGS[:-2]).encode())
+    return h.hexdigest()[:16]
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 

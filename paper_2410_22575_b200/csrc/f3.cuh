@@ -30,12 +30,13 @@
 
 namespace chessfad {
 
-// (A_kj, B_kj) sources: interleaved in shared memory (one 16-byte broadcast load), or the
+// (A_kj, B_kj) sources: interleaved and transposed in shared memory, abT[j*n + k] (one
+// 16-byte broadcast load; the KB k-values of one j sit at immediate offsets), or the
 // caller's params in global memory (two 8-byte broadcast loads through the read-only path)
 struct ABShared {
-  const double2* ab;
+  const double2* abT;
   int n;
-  CHF_INL double2 get(int k, int j) const { return ab[k * n + j]; }
+  CHF_INL double2 get(int k, int j) const { return abT[j * n + k]; }
 };
 struct ABGlobal {
   const double* A;

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(W * 32) hvp_reg_kernel(BatchArgs p) {
 // params = [A (n*n) | B (n*n) | E* (n)].  AB_SMEM: (A_kj, B_kj) interleaved into shared memory
 // (n <= 32), else read from params through the read-only path.
 template <int KB, bool HESS, bool AB_SMEM>
-__global__ void __launch_bounds__(kWarpsF3 * 32) hvp_f3_kernel(BatchArgs p) {
+__global__ void __launch_bounds__(kWarpsF3 * 32, 3) hvp_f3_kernel(BatchArgs p) {
   extern __shared__ double smem[];
   const int n = p.n, G = p.groups, P = 32 * G, C = p.csize;
   double* s_sa = smem;                 // [G][n][33]  sin a
@@ -126,7 +126,10 @@ __global__ void __launch_bounds__(kWarpsF3 * 32) hvp_f3_kernel(BatchArgs p) {
   const double* A = p.params;
   const double* B = p.params + (size_t)n * n;
   if (AB_SMEM)
-    for (int q = threadIdx.x; q < n * n; q += blockDim.x) s_ab[q] = make_double2(A[q], B[q]);
+    for (int q = threadIdx.x; q < n * n; q += blockDim.x) {
+      const int k = q / n, j = q - k * n;
+      s_ab[j * n + k] = make_double2(A[q], B[q]);  // transposed: [j][k]
+    }
   __syncthreads();
   // g, g', g'' of the seeded inputs: sin a_k, cos a_k once per tile (see f3.cuh)
   for (int q = threadIdx.x; q < G * n * 32; q += blockDim.x) {

@@ -40,6 +40,32 @@ def load(csv_path, order_path):
     return out
 
 
+def update_table(res, table_path):
+    """Merge executed-FLOP measurements into profiles/executed_flops.json (keyed by the
+    source hash of the build that was profiled)."""
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2410_22575_b200.build import source_hash
+    h = source_hash()
+    try:
+        tab = json.load(open(table_path))
+    except Exception:
+        tab = {}
+    if tab.get("src_hash") != h:
+        tab = {"src_hash": h, "entries": {}}
+    for r in res:
+        key = f"{r['func']} n={r['n']} C={r['C']}"
+        tab["entries"][key] = {"executed_flops_per_point": r["executed_flops"] / r["m"],
+                               "model_flops_per_point": r["model_flops"] / r["m"],
+                               "fp64_pipe_active_pct": r["fp64_pipe_active_pct"],
+                               "dram_bytes_per_launch": r["dram_bytes"], "m": r["m"], "regs": r["regs"],
+                               "ncu_time_ms": r["time_ms"]}
+    tab["note"] = ("executed FP64 FLOPs = 2*DFMA + DMUL + DADD thread instructions (ncu "
+                   "sm__sass_thread_inst_executed_op_{dfma,dmul,dadd}_pred_on.sum) per point, one launch each; "
+                   "tools/profile_sweep.py under ncu, summarised by tools/summarize_sweep.py")
+    json.dump(tab, open(table_path, "w"), indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
     res = load(sys.argv[1], sys.argv[2])
     print(f"{'func':16s} {'C':>3s} {'ms':>7s} {'exec/model':>10s} {'fp64pipe%':>9s} {'fl/inst':>7s} {'fp64share':>9s} {'DRAM MB':>8s} {'regs':>4s} {'warps%':>6s} {'GHz':>5s}")
@@ -49,3 +75,5 @@ if __name__ == "__main__":
               f"{r['warps_active_pct']:6.1f} {r['sm_clock_ghz']:5.2f}")
     if len(sys.argv) > 3:
         json.dump(res, open(sys.argv[3], "w"), indent=1)
+    if len(sys.argv) > 4:
+        update_table(res, sys.argv[4])
