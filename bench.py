@@ -157,8 +157,14 @@ def run_reference(args, rank, world):
 
 
 def workload_config(args, world):
-    return {"workload": f"cfg2: {args.func} n={args.n} C={args.csize} m={args.m} points per GPU (BASELINE configs[1])",
-            "func": args.func, "n": args.n, "csize": args.csize, "m_per_gpu": args.m, "global_points": args.m * world,
+    if getattr(args, "m_total", 0):
+        wl = f"cfg5: {args.func} n={args.n} C={args.csize} m={args.m_total} points over {world} GPU(s) (strong scaling)"
+        gp = args.m_total
+    else:
+        wl = f"cfg2: {args.func} n={args.n} C={args.csize} m={args.m} points per GPU (BASELINE configs[1])"
+        gp = args.m * world
+    return {"workload": wl,
+            "func": args.func, "n": args.n, "csize": args.csize, "m_per_gpu": args.m, "global_points": gp,
             "seed": 0, "parallelism": f"dp{world} (points sharded, no collective on the data path)",
             "l2": f"inputs larger than L2: {3 * args.m * args.n * 8 / 2**20:.0f} MiB per step vs 126 MB L2"}
 
@@ -173,7 +179,10 @@ def main():
     ap.add_argument("--func", choices=FUNCS, default="rosenbrock")
     ap.add_argument("--n", type=int, default=16)
     ap.add_argument("--csize", type=int, default=16)
-    ap.add_argument("--m", type=int, default=1 << 20)
+    ap.add_argument("--m", type=int, default=1 << 20, help="points per GPU (weak scaling)")
+    ap.add_argument("--m-total", type=int, default=0,
+                    help="strong scaling: total points split over the ranks (BASELINE cfg5: 8388608)")
+    ap.add_argument("--gather", action="store_true", help="time an all-gather of the results after the run")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -200,15 +209,19 @@ def main():
         if world > 1:
             dist.barrier()
 
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    from paper_2410_22575_b200.dist import gather_rows, max_over_ranks as _mor, shard
 
-    n, C, m = args.n, args.csize, args.m
-    first = rank * m
+    def max_over_ranks(x):
+        return _mor(x, device=dev)
+
+    n, C = args.n, args.csize
+    if args.m_total:
+        first, m = shard(args.m_total, rank, world)
+        m_all = args.m_total
+    else:
+        m = args.m
+        first, m_all = rank * m, world * m
+    args.m = m
     P = synth.points(0, n, m, first)
     V = synth.vectors(0, n, m, first)
     params_np = {f: (synth.fp_params_flat(0, n) if f == "fletcher_powell" else None) for f in FUNCS}
@@ -239,7 +252,7 @@ def main():
     sampler = ClockSampler(local)
     t = timed(args.func, C, args.steps, args.warmup, sampler)
     per_step = t / args.steps
-    value = world * m / per_step
+    value = m_all / per_step
     flops_pt = chf.model_flops_per_point(args.func, n, C)
     achieved_tf = m * flops_pt / per_step / 1e12  # per GPU, one launch per step
     clocks = sampler.summary()
@@ -280,7 +293,7 @@ def main():
         chf.hvp_batch_host(args.func, Ph, Vh, C, ph_params, out=Oh)  # synchronous
     e2e_t = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps)
     assert torch.equal(Oh, out.cpu()), "host-buffer path disagrees with the device path"
-    e2e = {"value": world * m / e2e_t, "unit": UNIT, "h2d_bytes_per_step": 2 * m * n * 8 + (
+    e2e = {"value": m_all / e2e_t, "unit": UNIT, "h2d_bytes_per_step": 2 * m * n * 8 + (
         0 if ph_params is None else ph_params.numel() * 8), "d2h_bytes_per_step": m * n * 8,
         "ms_per_step": e2e_t * 1e3, "api": "chessfad_hvp_batch_host (2-stream H2D/kernel/D2H pipeline)"}
 
@@ -297,7 +310,7 @@ def main():
                 tt = timed(f, c, ks, 3) / ks
                 fl = chf.model_flops_per_point(f, n, c)
                 exs = executed_entry(f, n, c, src_hash)
-                sweep.append({"func": f, "csize": c, "hvp_per_s": world * m / tt, "ms": tt * 1e3,
+                sweep.append({"func": f, "csize": c, "hvp_per_s": m_all / tt, "ms": tt * 1e3,
                               "model_tflops_effective": m * fl / tt / 1e12,
                               "executed_tflops": None if exs is None else m * exs["executed_flops_per_point"] / tt / 1e12,
                               "executed_frac": None if exs is None else
@@ -327,10 +340,24 @@ def main():
         accounting = "executed-FLOP table missing or stale for this build: achieved = model FLOPs (effective)"
     achieved = exec_tf if exec_tf is not None else model_tf
 
+    gather = None
+    if args.gather:
+        torch.cuda.synchronize()
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        full = gather_rows(out, m_all)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gather = {"ms": max_over_ranks(g0.elapsed_time(g1)), "bytes_per_rank": int(full.numel() * 8),
+                  "collective": "all_gather (NCCL)" if world > 1 else "none (1 rank)"}
+        del full
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
+            "scaling": "strong" if args.m_total else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_config(args, world),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf, "traffic": traffic, "accounting": accounting,
@@ -344,7 +371,7 @@ def main():
                          "model_flops_per_point": flops_pt,
                          "fp64_probe_tflops": probe_tf, "frac_of_probe": achieved / probe_tf},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps, "clocks": clocks, "parity": parity,
-            "sweep": sweep,
+            "gather": gather, "sweep": sweep,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -76,6 +76,25 @@ int chessfad_hessian_batch(int func, int n, int csize, int64_t m, const double *
                            const double *params, void *stream);
 
 /*
+ * Symmetric chunked HVP, Alg 8 SC-HESS-VEC (§III-C): for row
+ * i only chunks cn >= i/csize are evaluated (n(n/C+1)/2 evaluations per point);
+ * each entry H_is of a chunk strictly after row i's chunk also adds H_is*vecs[i] to out[s].
+ * Reading of the garbled loop bound (G8): all csize second-order slots are used and
+ * out <- res.  Same arguments, layout and semantics as chessfad_hvp_batch.
+ */
+int chessfad_sym_hvp_batch(int func, int n, int csize, int64_t m, const double *points, const double *vecs,
+                           double *out, const double *params, void *stream);
+
+/*
+ * Symmetric chunked Hessian, Alg 6 SCHUNK-HESS: chunks cn >= i/csize are
+ * evaluated and stored; whole chunks strictly below row i's chunk are mirrored
+ * (hess[e][s][i] = hess[e][i][s]); entries of the diagonal chunk are computed directly (mirror
+ * loop read as exclusive of endindex, G9).  Same arguments as chessfad_hessian_batch.
+ */
+int chessfad_sym_hessian_batch(int func, int n, int csize, int64_t m, const double *points, double *hess,
+                               const double *params, void *stream);
+
+/*
  * End-to-end variant of chessfad_hvp_batch on HOST buffers: points, vecs, out (m x n) and
  * params are HOST pointers (pinned memory gives copy/compute overlap; pageable memory
  * works but serialises).  The batch is split into pieces of `piece_points` points
@@ -87,8 +106,24 @@ int chessfad_hessian_batch(int func, int n, int csize, int64_t m, const double *
 int chessfad_hvp_batch_host(int func, int n, int csize, int64_t m, const double *points, const double *vecs,
                             double *out, const double *params, int64_t piece_points, void *stream);
 
-/* 1 if (func, n, csize) has a compiled kernel, else 0 (argument errors also give 0). */
+/* 1 if (func, n, csize) runs for both chessfad_hvp_batch and chessfad_hessian_batch, else 0
+ * (argument errors also give 0).  Compiled set: Fletcher-
+ * Powell any csize | n, n <= 128; the other functions n <= 256 (Ackley n <= 160), with one
+ * hDual<csize> per evaluation for csize in {1,2,4,8,16,32} and, for any other csize | n, csize/c'
+ * column groups of the largest c' in {1,2,4,8,16} dividing csize (bit-identical results by
+ * slot independence; slots 0/1 recomputed per group). */
 int chessfad_is_supported(int func, int n, int csize);
+
+/* algorithm ids for chessfad_is_supported_algo / chessfad_model_flops_per_point_algo */
+enum chessfad_algo {
+  CHESSFAD_ALGO_HVP = 0,          /* Alg 7, chessfad_hvp_batch */
+  CHESSFAD_ALGO_HESSIAN = 1,      /* Alg 5, chessfad_hessian_batch */
+  CHESSFAD_ALGO_SYM_HVP = 2,      /* Alg 8, chessfad_sym_hvp_batch */
+  CHESSFAD_ALGO_SYM_HESSIAN = 3   /* Alg 6, chessfad_sym_hessian_batch */
+};
+
+/* 1 if (func, n, csize) runs for the given algorithm, else 0. */
+int chessfad_is_supported_algo(int func, int n, int csize, int algo);
 
 /* Static description of a status code. */
 const char *chessfad_status_string(int status);
@@ -101,6 +136,11 @@ const char *chessfad_status_string(int status);
  * Returns -1 on invalid arguments.
  */
 double chessfad_model_flops_per_point(int func, int n, int csize, int hessian);
+
+/* Model FLOPs per point for any algorithm id: evaluations (n^2/C for Alg 5/7, n(n/C+1)/2 for
+ * Alg 6/8) x per-evaluation cost, plus 2n^2 for the HVP algorithms (Alg 8's
+ * n(n+C)/2 direct and n(n-C)/2 mirrored terms also total n^2 multiply-adds). */
+double chessfad_model_flops_per_point_algo(int func, int n, int csize, int algo);
 
 /*
  * FP64 pipe probe: launches `blocks` x 256 threads, each running `iters` iterations of one

@@ -18,8 +18,11 @@ ROSENBROCK, ACKLEY, FLETCHER_POWELL, PRODSUM = 0, 1, 2, 3
 FUNCS = {"rosenbrock": ROSENBROCK, "ackley": ACKLEY, "fletcher_powell": FLETCHER_POWELL, "prodsum": PRODSUM}
 STATUS = {0: "CHESSFAD_OK", 1: "CHESSFAD_ERR_ARG", 2: "CHESSFAD_ERR_CHUNK", 3: "CHESSFAD_ERR_FUNC",
           4: "CHESSFAD_ERR_UNSUPPORTED", 5: "CHESSFAD_ERR_CUDA"}
-EXPORTS = ["chessfad_hvp_batch", "chessfad_hessian_batch", "chessfad_hvp_batch_host", "chessfad_is_supported",
-           "chessfad_status_string", "chessfad_model_flops_per_point", "chessfad_fp64_probe", "chessfad_version"]
+ALGOS = {"hvp": 0, "hessian": 1, "sym_hvp": 2, "sym_hessian": 3}
+EXPORTS = sorted(["chessfad_hvp_batch", "chessfad_hessian_batch", "chessfad_sym_hvp_batch", "chessfad_sym_hessian_batch",
+                  "chessfad_hvp_batch_host", "chessfad_is_supported", "chessfad_is_supported_algo",
+                  "chessfad_status_string", "chessfad_model_flops_per_point", "chessfad_model_flops_per_point_algo",
+                  "chessfad_fp64_probe", "chessfad_version"])
 
 _lock = threading.Lock()
 _lib = None
@@ -47,6 +50,10 @@ def load(build_if_missing: bool = True):
         sig = {
             "chessfad_hvp_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_hessian_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
+            "chessfad_sym_hvp_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
+            "chessfad_sym_hessian_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
+            "chessfad_is_supported_algo": (i32, [i32, i32, i32, i32]),
+            "chessfad_model_flops_per_point_algo": (dbl, [i32, i32, i32, i32]),
             "chessfad_hvp_batch_host": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, i64, vp]),
             "chessfad_is_supported": (i32, [i32, i32, i32]),
             "chessfad_status_string": (ctypes.c_char_p, [i32]),
@@ -88,31 +95,49 @@ def _dev(t, name, shape=None):
     return ctypes.c_void_p(t.data_ptr())
 
 
-def hvp_batch(func, points, vecs, csize: int, params=None, out=None, stream=None):
-    """out[e] = Hess f(points[e]) @ vecs[e] for every row e (Alg 7, batched).
-
-    points, vecs: (m, n) float64 CUDA tensors; params: (2n^2+n,) float64 CUDA tensor for
-    Fletcher-Powell.  Asynchronous on `stream` (default: torch's current stream)."""
+def _hvp(entry, func, points, vecs, csize, params, out, stream):
     import torch
     m, n = points.shape
     if out is None:
         out = torch.empty_like(points)
-    st = load().chessfad_hvp_batch(_func(func), n, csize, m, _dev(points, "points"), _dev(vecs, "vecs", (m, n)),
-                                   _dev(out, "out", (m, n)), _dev(params, "params"), _stream_ptr(stream))
+    st = getattr(load(), entry)(_func(func), n, csize, m, _dev(points, "points"), _dev(vecs, "vecs", (m, n)),
+                                _dev(out, "out", (m, n)), _dev(params, "params"), _stream_ptr(stream))
     _check(st)
     return out
 
 
-def hessian_batch(func, points, csize: int, params=None, out=None, stream=None):
-    """hess[e] = Hess f(points[e]), every entry computed (Alg 5, batched): (m, n, n)."""
+def _hess(entry, func, points, csize, params, out, stream):
     import torch
     m, n = points.shape
     if out is None:
         out = torch.empty((m, n, n), dtype=torch.float64, device=points.device)
-    st = load().chessfad_hessian_batch(_func(func), n, csize, m, _dev(points, "points"), _dev(out, "hess", (m, n, n)),
-                                       _dev(params, "params"), _stream_ptr(stream))
+    st = getattr(load(), entry)(_func(func), n, csize, m, _dev(points, "points"), _dev(out, "hess", (m, n, n)),
+                                _dev(params, "params"), _stream_ptr(stream))
     _check(st)
     return out
+
+
+def hvp_batch(func, points, vecs, csize: int, params=None, out=None, stream=None):
+    """out[e] = Hess f(points[e]) @ vecs[e] for every row e (Alg 7 CHESS-VEC, batched).
+
+    points, vecs: (m, n) float64 CUDA tensors; params: (2n^2+n,) float64 CUDA tensor for
+    Fletcher-Powell.  Asynchronous on `stream` (default: torch's current stream)."""
+    return _hvp("chessfad_hvp_batch", func, points, vecs, csize, params, out, stream)
+
+
+def sym_hvp_batch(func, points, vecs, csize: int, params=None, out=None, stream=None):
+    """Same product with the symmetric chunked algorithm (Alg 8 SC-HESS-VEC, batched)."""
+    return _hvp("chessfad_sym_hvp_batch", func, points, vecs, csize, params, out, stream)
+
+
+def hessian_batch(func, points, csize: int, params=None, out=None, stream=None):
+    """hess[e] = Hess f(points[e]), every entry computed (Alg 5 CHUNK-HESS, batched): (m, n, n)."""
+    return _hess("chessfad_hessian_batch", func, points, csize, params, out, stream)
+
+
+def sym_hessian_batch(func, points, csize: int, params=None, out=None, stream=None):
+    """Hessians by Alg 6 SCHUNK-HESS: upper chunks computed, whole lower chunks mirrored."""
+    return _hess("chessfad_sym_hessian_batch", func, points, csize, params, out, stream)
 
 
 def _host_ptr(x, name, writable=False):
@@ -146,12 +171,16 @@ def hvp_batch_host(func, points, vecs, csize: int, params=None, out=None, piece_
     return out
 
 
-def is_supported(func, n: int, csize: int) -> bool:
-    return bool(load().chessfad_is_supported(_func(func), n, csize))
+def is_supported(func, n: int, csize: int, algo: str | None = None) -> bool:
+    if algo is None:
+        return bool(load().chessfad_is_supported(_func(func), n, csize))
+    return bool(load().chessfad_is_supported_algo(_func(func), n, csize, ALGOS[algo]))
 
 
-def model_flops_per_point(func, n: int, csize: int, hessian: bool = False) -> float:
-    return float(load().chessfad_model_flops_per_point(_func(func), n, csize, int(hessian)))
+def model_flops_per_point(func, n: int, csize: int, hessian: bool = False, algo: str | None = None) -> float:
+    if algo is None:
+        return float(load().chessfad_model_flops_per_point(_func(func), n, csize, int(hessian)))
+    return float(load().chessfad_model_flops_per_point_algo(_func(func), n, csize, ALGOS[algo]))
 
 
 def fp64_probe(blocks: int, iters: int, sink, stream=None):

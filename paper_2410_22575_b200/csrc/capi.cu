@@ -12,15 +12,6 @@
 
 using namespace chessfad;
 
-namespace chessfad {
-int reg_warps() {
-  static const int w = [] {
-    const char* e = getenv("CHESSFAD_REG_WARPS");
-    return (e && atoi(e) == 8) ? 8 : 4;
-  }();
-  return w;
-}
-}  // namespace chessfad
 
 namespace {
 
@@ -28,6 +19,18 @@ constexpr int kMaxNReg = 256;  // register-hDual path: (3 or 5)*n*33*8 B of shar
 constexpr int kMaxNF3 = 128;   // F3 path: per-thread R0/R1 scratch of 128 doubles
 
 bool reg_chunk_compiled(int C) { return C == 1 || C == 2 || C == 4 || C == 8 || C == 16 || C == 32; }
+
+// Register path, C outside the compiled set: the chunk is executed as C/c' column groups of
+// the largest compiled c' <= 16 dividing C.  By slot independence column k of a
+// hDual<C> evaluation is bit-identical to column k of a hDual<c'> evaluation with the same
+// row seed, so the results are those of hDual<C>; slots 0 and 1 are recomputed per group
+// (executed FLOPs > model FLOPs, never fewer).
+int reg_kernel_chunk(int C) {
+  if (reg_chunk_compiled(C)) return C;
+  for (int c = 16; c > 1; c >>= 1)
+    if (C % c == 0) return c;
+  return 1;
+}
 
 int validate(int func, int n, int csize, int64_t m, bool need_params_ptr, const void* params,
              const void* p1, const void* p2, const void* p3) {
@@ -50,11 +53,14 @@ int validate(int func, int n, int csize, int64_t m, bool need_params_ptr, const 
   return CHESSFAD_OK;
 }
 
-int supported(int func, int n, int csize) {
-  if (func == CHESSFAD_FLETCHER_POWELL) return n <= kMaxNF3;
+constexpr size_t kSmemMax = 227 * 1024;
+
+int supported(int func, int n, int csize, int mode) {
+  (void)csize;  // every C | n runs (F3: runtime C; register path: reg_kernel_chunk)
+  if (func == CHESSFAD_FLETCHER_POWELL)
+    return n <= kMaxNF3 && f3_smem_bytes(n, groups_for(n, kWarpsF3, mode), mode) <= kSmemMax;
   const int fn = func == CHESSFAD_ACKLEY ? FUNC_ACKLEY : FUNC_ROSENBROCK;
-  const size_t smem = std::max(reg_smem_bytes(fn, n, groups_for(n, 4), false), reg_smem_bytes(fn, n, groups_for(n, 8), false));
-  return n <= kMaxNReg && smem <= 227 * 1024 && reg_chunk_compiled(csize);
+  return n <= kMaxNReg && reg_smem_bytes(fn, n, groups_for(n, kWarpsReg, mode), mode) <= kSmemMax;
 }
 
 // largest power of two <= 16 that divides n: the F3 k-block
@@ -64,16 +70,17 @@ int f3_kb(int n) {
   return kb;
 }
 
-template <bool HESS>
-cudaError_t dispatch_reg(int func, int C, const BatchArgs& a, cudaStream_t s) {
+template <int MODE>
+cudaError_t dispatch_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s) {
+  const int C = reg_kernel_chunk(Capi);
 #define CHF_CASE_C(F)                                  \
   switch (C) {                                         \
-    case 1: return launch_reg<F, 1, HESS>(a, s);       \
-    case 2: return launch_reg<F, 2, HESS>(a, s);       \
-    case 4: return launch_reg<F, 4, HESS>(a, s);       \
-    case 8: return launch_reg<F, 8, HESS>(a, s);       \
-    case 16: return launch_reg<F, 16, HESS>(a, s);     \
-    case 32: return launch_reg<F, 32, HESS>(a, s);     \
+    case 1: return launch_reg<F, 1, MODE>(a, s);       \
+    case 2: return launch_reg<F, 2, MODE>(a, s);       \
+    case 4: return launch_reg<F, 4, MODE>(a, s);       \
+    case 8: return launch_reg<F, 8, MODE>(a, s);       \
+    case 16: return launch_reg<F, 16, MODE>(a, s);     \
+    case 32: return launch_reg<F, 32, MODE>(a, s);     \
   }                                                    \
   break;
   switch (func) {
@@ -85,11 +92,11 @@ cudaError_t dispatch_reg(int func, int C, const BatchArgs& a, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
-template <bool HESS>
+template <int MODE>
 cudaError_t dispatch_f3(const BatchArgs& a, cudaStream_t s) {
-  const bool ab_smem = a.n <= 32;
+  const bool ab_smem = f3_ab_smem(a.n);
 #define CHF_CASE_KB(KB) \
-  case KB: return ab_smem ? launch_f3<KB, HESS, true>(a, s) : launch_f3<KB, HESS, false>(a, s);
+  case KB: return ab_smem ? launch_f3<KB, MODE, true>(a, s) : launch_f3<KB, MODE, false>(a, s);
   switch (f3_kb(a.n)) {
     CHF_CASE_KB(1) CHF_CASE_KB(2) CHF_CASE_KB(4) CHF_CASE_KB(8) CHF_CASE_KB(16)
   }
@@ -97,7 +104,7 @@ cudaError_t dispatch_f3(const BatchArgs& a, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
-template <bool HESS>
+template <int MODE>
 int run(int func, int n, int csize, int64_t m, const double* points, const double* vecs, double* out,
         const double* params, cudaStream_t s) {
   BatchArgs a;
@@ -109,8 +116,19 @@ int run(int func, int n, int csize, int64_t m, const double* points, const doubl
   a.vecs = vecs;
   a.out = out;
   a.params = params;
-  const cudaError_t e = (func == CHESSFAD_FLETCHER_POWELL) ? dispatch_f3<HESS>(a, s) : dispatch_reg<HESS>(func, csize, a, s);
+  const cudaError_t e = (func == CHESSFAD_FLETCHER_POWELL) ? dispatch_f3<MODE>(a, s) : dispatch_reg<MODE>(func, csize, a, s);
   return e == cudaSuccess ? CHESSFAD_OK : CHESSFAD_ERR_CUDA;
+}
+
+template <int MODE>
+int batch_entry(int func, int n, int csize, int64_t m, const double* points, const double* vecs, double* out,
+                const double* params, void* stream) {
+  const bool hess = mode_hess(MODE);
+  int st = validate(func, n, csize, m, false, params, points, hess ? out : vecs, out);
+  if (st) return st;
+  if (!supported(func, n, csize, MODE)) return CHESSFAD_ERR_UNSUPPORTED;
+  if (m == 0) return CHESSFAD_OK;
+  return run<MODE>(func, n, csize, m, points, vecs, out, params, (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------- FP64 probe kernel
@@ -130,27 +148,29 @@ extern "C" {
 
 int chessfad_hvp_batch(int func, int n, int csize, int64_t m, const double* points, const double* vecs, double* out,
                        const double* params, void* stream) {
-  int st = validate(func, n, csize, m, false, params, points, vecs, out);
-  if (st) return st;
-  if (!supported(func, n, csize)) return CHESSFAD_ERR_UNSUPPORTED;
-  if (m == 0) return CHESSFAD_OK;
-  return run<false>(func, n, csize, m, points, vecs, out, params, (cudaStream_t)stream);
+  return batch_entry<MODE_HVP>(func, n, csize, m, points, vecs, out, params, stream);
 }
 
 int chessfad_hessian_batch(int func, int n, int csize, int64_t m, const double* points, double* hess,
                            const double* params, void* stream) {
-  int st = validate(func, n, csize, m, false, params, points, hess, hess);
-  if (st) return st;
-  if (!supported(func, n, csize)) return CHESSFAD_ERR_UNSUPPORTED;
-  if (m == 0) return CHESSFAD_OK;
-  return run<true>(func, n, csize, m, points, nullptr, hess, params, (cudaStream_t)stream);
+  return batch_entry<MODE_HESS>(func, n, csize, m, points, nullptr, hess, params, stream);
+}
+
+int chessfad_sym_hvp_batch(int func, int n, int csize, int64_t m, const double* points, const double* vecs,
+                           double* out, const double* params, void* stream) {
+  return batch_entry<MODE_SYM_HVP>(func, n, csize, m, points, vecs, out, params, stream);
+}
+
+int chessfad_sym_hessian_batch(int func, int n, int csize, int64_t m, const double* points, double* hess,
+                               const double* params, void* stream) {
+  return batch_entry<MODE_SYM_HESS>(func, n, csize, m, points, nullptr, hess, params, stream);
 }
 
 int chessfad_hvp_batch_host(int func, int n, int csize, int64_t m, const double* points, const double* vecs,
                             double* out, const double* params, int64_t piece_points, void* stream) {
   int st = validate(func, n, csize, m, false, params, points, vecs, out);
   if (st) return st;
-  if (!supported(func, n, csize)) return CHESSFAD_ERR_UNSUPPORTED;
+  if (!supported(func, n, csize, MODE_HVP)) return CHESSFAD_ERR_UNSUPPORTED;
   if (m == 0) return CHESSFAD_OK;
   cudaStream_t s0 = (cudaStream_t)stream;
   if (piece_points <= 0) piece_points = std::max<int64_t>(4096, (m + 7) / 8);
@@ -191,7 +211,7 @@ int chessfad_hvp_batch_host(int func, int n, int csize, int64_t m, const double*
       ok(cudaMemcpyAsync(dp, points + e0 * n, bytes, cudaMemcpyHostToDevice, s));
       ok(cudaMemcpyAsync(dv, vecs + e0 * n, bytes, cudaMemcpyHostToDevice, s));
       if (e == cudaSuccess) {
-        const int r = run<false>(func, n, csize, cnt, dp, dv, dout, nparams ? d_params : nullptr, s);
+        const int r = run<MODE_HVP>(func, n, csize, cnt, dp, dv, dout, nparams ? d_params : nullptr, s);
         if (r != CHESSFAD_OK) e = cudaErrorLaunchFailure;
       }
       ok(cudaMemcpyAsync(out + e0 * n, dout, bytes, cudaMemcpyDeviceToHost, s));
@@ -215,7 +235,16 @@ int chessfad_is_supported(int func, int n, int csize) {
   if (validate(func, n, csize, 0, false, func == CHESSFAD_FLETCHER_POWELL ? (const void*)1 : nullptr, nullptr,
                nullptr, nullptr))
     return 0;
-  return supported(func, n, csize);
+  return supported(func, n, csize, MODE_HVP) && supported(func, n, csize, MODE_HESS);
+}
+
+int chessfad_is_supported_algo(int func, int n, int csize, int algo) {
+  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_SYM_HESSIAN) return 0;
+  if (validate(func, n, csize, 0, false, func == CHESSFAD_FLETCHER_POWELL ? (const void*)1 : nullptr, nullptr,
+               nullptr, nullptr))
+    return 0;
+  static const int mode_of[4] = {MODE_HVP, MODE_HESS, MODE_SYM_HVP, MODE_SYM_HESS};
+  return supported(func, n, csize, mode_of[algo]);
 }
 
 const char* chessfad_status_string(int status) {
@@ -230,7 +259,8 @@ const char* chessfad_status_string(int status) {
   return "CHESSFAD: unknown status";
 }
 
-double chessfad_model_flops_per_point(int func, int n, int csize, int hessian) {
+double chessfad_model_flops_per_point_algo(int func, int n, int csize, int algo) {
+  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_SYM_HESSIAN) return -1.0;
   if (validate(func, n, csize, 0, false, (const void*)1, nullptr, nullptr, nullptr)) return -1.0;
   const double C = csize, N = n;
   // per-evaluation hDual op counts of the canonical forms (DESIGN.md op table)
@@ -242,7 +272,15 @@ double chessfad_model_flops_per_point(int func, int n, int csize, int hessian) {
     case CHESSFAD_PRODSUM: hm = N - 1; ha = N - 2; break;
   }
   const double per_eval = hm * (10 * C + 4) + ha * (2 * C + 2) + sm * (2 * C + 2) + sa + un * (4 * C + 2);
-  return (N * N / C) * per_eval + (hessian ? 0.0 : 2 * N * N);
+  const bool sym = algo == CHESSFAD_ALGO_SYM_HVP || algo == CHESSFAD_ALGO_SYM_HESSIAN;
+  const double evals = sym ? N * (N / C + 1) / 2 : N * N / C;
+  // HVP dot: every H_ij v_j term once (Alg 8: n(n+C)/2 direct + n(n-C)/2 mirrored) = 2n^2
+  const bool hvp = algo == CHESSFAD_ALGO_HVP || algo == CHESSFAD_ALGO_SYM_HVP;
+  return evals * per_eval + (hvp ? 2 * N * N : 0.0);
+}
+
+double chessfad_model_flops_per_point(int func, int n, int csize, int hessian) {
+  return chessfad_model_flops_per_point_algo(func, n, csize, hessian ? CHESSFAD_ALGO_HESSIAN : CHESSFAD_ALGO_HVP);
 }
 
 int chessfad_fp64_probe(int blocks, int64_t iters, double* sink, void* stream) {

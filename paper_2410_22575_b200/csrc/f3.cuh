@@ -62,16 +62,15 @@ CHF_INL void f3_accum(const AB& ab, int kb, int j, double sp, double cp, double 
   }
 }
 
-// One evaluation f<hDual<C>>(CHUNK-INIT(i, cs)) for this lane's point (Alg 7 :389-394).
-//   HVP:     returns res + sum_l d2f/dx_i dx_{cs+l} * v[cs+l], accumulated in ascending l
-//   Hessian: writes d2f/dx_i dx_{cs+l} to hrow[cs+l] (when hrow != nullptr)
-// sa/ca: sin/cos of the lane's coordinates, element j at [j * stride]; Es: E*;
-// v: the lane's vector, element j at [j * stride].  R0/R1: per-thread scratch (n doubles).
-template <int KB, bool HESS, class AB>
-CHF_INL double f3_eval(int n, int C, int i, int cs, const double* __restrict__ sa,
-                       const double* __restrict__ ca, int stride, const AB& ab,
-                       const double* __restrict__ Es, const double* __restrict__ v,
-                       double* __restrict__ hrow, double* R0, double* R1, double res) {
+// One evaluation f<hDual<C>>(CHUNK-INIT(i, cs)) for this lane's point (Alg 4 + Fig. 1).
+// For each column l in ascending order, sink(cs + l, d2f/dx_i dx_{cs+l}) consumes the
+// second-order slot C+2+l (the chunk dot of Alg 7, the store of Alg 5, the scatter of Alg 8).
+// sa/ca: sin/cos of the lane's coordinates, element j at [j * stride]; Es: E*.
+// R0/R1: per-thread scratch (n doubles).
+template <int KB, class AB, class Sink>
+CHF_INL void f3_eval(int n, int C, int i, int cs, const double* __restrict__ sa,
+                     const double* __restrict__ ca, int stride, const AB& ab,
+                     const double* __restrict__ Es, double* R0, double* R1, Sink&& sink) {
   // ---------------- phase A: slots 0 and 1
   for (int kb = 0; kb < n; kb += KB) {
     double E0[KB], E1[KB];
@@ -125,13 +124,8 @@ CHF_INL double f3_eval(int n, int C, int i, int cs, const double* __restrict__ s
         fC = (k == 0) ? rrC : fC + rrC;
       }
     }
-    if (HESS) {
-      if (hrow) hrow[col] = fC;
-    } else {
-      res = res + fC * v[col * stride];
-    }
+    sink(col, fC);
   }
-  return res;
 }
 
 }  // namespace chessfad

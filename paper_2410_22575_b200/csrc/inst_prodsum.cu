@@ -1,9 +1,9 @@
-// inst_prodsum.cu -- kernel instantiations for FUNC_PRODSUM (hDual<C> in registers), C in {1..32}.
+// inst_prodsum.cu -- kernel instantiations for FUNC_PRODSUM (hDual<C> in registers), C in {1..32},
+// all four modes (Alg 7, Alg 5, Alg 8, Alg 6).
 #include "launch.cuh"
 
 namespace chessfad {
-#define CHF_INST_REG(F, C)                                                 \
-  template cudaError_t launch_reg<F, C, false>(BatchArgs, cudaStream_t); \
-  template cudaError_t launch_reg<F, C, true>(BatchArgs, cudaStream_t);
+#define CHF_INST_REG1(F, C, M) template cudaError_t launch_reg<F, C, M>(BatchArgs, cudaStream_t);
+#define CHF_INST_REG(F, C) CHF_FOR_MODE(CHF_INST_REG1, F, C)
 CHF_FOR_C(CHF_INST_REG, FUNC_PRODSUM)
 }  // namespace chessfad

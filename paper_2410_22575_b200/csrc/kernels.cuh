@@ -5,12 +5,23 @@
 // shared-memory reduction).  Here a LANE is a POINT and a WARP is a ROW:
 //   * the 32 lanes of a warp hold 32 different points and evaluate the SAME (row i,
 //     chunk cs) -> CHUNK-INIT seeds, loop bounds and control flow are warp-uniform;
-//   * a thread loops over the n/C chunks of its row and accumulates the row of H.v in a
+//   * a thread loops over the chunks of its row and accumulates the row of H.v in a
 //     register in ascending chunk order (Alg 7 order; no reduction across threads);
 //   * a CTA stages a tile of 32*G points (and vectors) once, transposed [k][lane] in
 //     shared memory (stride 33: conflict-free), with coalesced global loads; its warps
 //     share the tile and split the n rows; the output tile is written back coalesced.
 // Inputs are m x n FP64 row-major, instance-major a[e*n + k].
+//
+// Modes (one kernel body, the consumer of each finished column differs):
+//   MODE_HVP       Alg 7 CHESS-VEC  out[i] = sum over all chunks
+//   MODE_HESS      Alg 5 CHUNK-HESS  H[i][cs+l] stored
+//   MODE_SYM_HVP   Alg 8 SC-HESS-VEC  chunks cn >= i/C only; H_is v_i also
+//                  scattered into out[s] for chunks after row i's (reading G8)
+//   MODE_SYM_HESS  Alg 6 SCHUNK-HESS  chunks cn >= i/C only, mirrored
+// The symmetric modes use the API chunk size p.csize to decide which chunks are computed
+// (the kernel's register chunk C may be a column group of it).  MODE_SYM_HVP needs one
+// thread to own all rows of its point (the scatter crosses rows), so its CTA holds W groups
+// of 32 points and every warp walks all n rows of its own group (the paper's L0 level).
 #pragma once
 #include <cstdint>
 
@@ -19,9 +30,13 @@
 
 namespace chessfad {
 
+enum { MODE_HVP = 0, MODE_HESS = 1, MODE_SYM_HVP = 2, MODE_SYM_HESS = 3 };
+__host__ __device__ constexpr bool mode_hess(int M) { return M == MODE_HESS || M == MODE_SYM_HESS; }
+__host__ __device__ constexpr bool mode_sym(int M) { return M == MODE_SYM_HVP || M == MODE_SYM_HESS; }
+
 struct BatchArgs {
   int n;
-  int csize;
+  int csize;   // the API chunk size C (symmetric modes: which chunks are computed)
   int groups;  // G: 32-point groups per CTA
   int64_t m;
   const double* __restrict__ points;
@@ -30,8 +45,8 @@ struct BatchArgs {
   const double* __restrict__ params;
 };
 
-constexpr int kPad = 33;          // shared-memory row stride (doubles) of [k][lane] tiles
-constexpr int kWarpsF3 = 4;       // Fletcher-Powell path: 128 threads per CTA
+constexpr int kPad = 33;     // shared-memory row stride (doubles) of [k][lane] tiles
+constexpr int kWarpsF3 = 4;  // Fletcher-Powell path: 128 threads per CTA
 
 // stage points [and vectors] of the tile into shared memory, transposed per 32-point group
 CHF_INL void stage_tile(const BatchArgs& p, int64_t e0, int P, double* s_pts, double* s_vec) {
@@ -55,11 +70,51 @@ CHF_INL void write_tile(const BatchArgs& p, int64_t e0, int P, const double* s_o
   }
 }
 
+// Per-row consumer of finished columns (one instance per thread and row).
+//   a5/a6 of §8(a): res accumulates sum_l H[i][col] * v[col] in ascending column order.
+template <int MODE>
+struct RowSink {
+  double res;       // HVP modes: this row's accumulator
+  const double* v;  // lane's vector column (stride kPad), HVP modes
+  double* s_res;    // lane's output column (stride kPad), MODE_SYM_HVP scatter target
+  double vi;        // v[i], MODE_SYM_HVP
+  double* hrow;     // &H[e][i][0] (nullptr for ragged-tail lanes), Hessian modes
+  double* hcol;     // &H[e][0][i] (stride n), MODE_SYM_HESS mirror
+  int n;
+  bool mirror;      // symmetric modes: this chunk lies strictly after row i's chunk
+  CHF_INL void operator()(int col, double h) {
+    if (MODE == MODE_HVP || MODE == MODE_SYM_HVP) {
+      res = res + h * v[col * kPad];
+      if (MODE == MODE_SYM_HVP && mirror) s_res[col * kPad] = s_res[col * kPad] + h * vi;
+    } else if (hrow) {
+      hrow[col] = h;
+      if (MODE == MODE_SYM_HESS && mirror) hcol[(size_t)col * n] = h;
+    }
+  }
+};
+
+template <int MODE>
+CHF_INL RowSink<MODE> make_sink(const BatchArgs& p, int i, int64_t e, const double* v, double* o) {
+  constexpr bool HESS = mode_hess(MODE);
+  const int n = p.n;
+  RowSink<MODE> s;
+  s.res = MODE == MODE_SYM_HVP ? o[i * kPad] : 0.0;
+  s.v = v;
+  s.s_res = o;
+  s.vi = HESS ? 0.0 : v[i * kPad];
+  s.hrow = (HESS && e < p.m) ? p.out + (e * n + i) * n : nullptr;
+  s.hcol = (HESS && e < p.m) ? p.out + e * n * n + i : nullptr;
+  s.n = n;
+  s.mirror = false;
+  return s;
+}
+
 // ---------------------------------------------------------------- F1, F2, F4: hDual<C> in registers
-template <int FUNC, int C, bool HESS, int W>
+template <int FUNC, int C, int MODE, int W>
 __global__ void __launch_bounds__(W * 32) hvp_reg_kernel(BatchArgs p) {
+  constexpr bool HESS = mode_hess(MODE);
   extern __shared__ double smem[];
-  const int n = p.n, G = p.groups, P = 32 * G;
+  const int n = p.n, G = p.groups, P = 32 * G, Capi = p.csize;
   double* s_pts = smem;
   double* s_vec = HESS ? nullptr : s_pts + G * n * kPad;
   double* s_out = HESS ? nullptr : s_vec + G * n * kPad;
@@ -67,6 +122,8 @@ __global__ void __launch_bounds__(W * 32) hvp_reg_kernel(BatchArgs p) {
   double* s_cos = s_sin + G * n * kPad;
   const int64_t e0 = (int64_t)blockIdx.x * P;
   stage_tile(p, e0, P, s_pts, s_vec);
+  if (MODE == MODE_SYM_HVP)
+    for (int q = threadIdx.x; q < G * n * kPad; q += blockDim.x) s_out[q] = 0.0;
   if (FUNC == FUNC_ACKLEY) {
     __syncthreads();
     for (int q = threadIdx.x; q < G * n * 32; q += blockDim.x) {
@@ -80,28 +137,23 @@ __global__ void __launch_bounds__(W * 32) hvp_reg_kernel(BatchArgs p) {
   const int g = warp % G, rstep = W / G;
   const double* a = s_pts + g * n * kPad + lane;
   const double* v = HESS ? nullptr : s_vec + g * n * kPad + lane;
+  double* o = HESS ? nullptr : s_out + g * n * kPad + lane;
   const double* tsin = FUNC == FUNC_ACKLEY ? s_sin + g * n * kPad + lane : nullptr;
   const double* tcos = FUNC == FUNC_ACKLEY ? s_cos + g * n * kPad + lane : nullptr;
   const int64_t e = e0 + g * 32 + lane;
   const int nchunk = n / C;
   for (int i = warp / G; i < n; i += rstep) {
-    double res = 0.0;
-    for (int j = 0; j < nchunk; j++) {
+    const int scn = i / Capi;  // row i's first chunk (symmetric modes)
+    RowSink<MODE> sink = make_sink<MODE>(p, i, e, v, o);
+    for (int j = mode_sym(MODE) ? (scn * Capi) / C : 0; j < nchunk; j++) {
       const int cs = j * C;
+      sink.mirror = cs / Capi > scn;
       const LaneSeed<C> y{a, kPad, i, cs, tsin, tcos};
       const hd<C> t = eval_f<FUNC, C>(n, y);  // CHUNK-INIT + f<hDual<C>>, Alg 7 :389-390
-      if (HESS) {
-        if (e < p.m) {
-          double* h = p.out + (e * n + i) * n + cs;  // H[e][i][cs + l] = t.v[C+2+l] (Alg 5)
 #pragma unroll
-          for (int l = 0; l < C; l++) h[l] = t.v[C + 2 + l];
-        }
-      } else {
-#pragma unroll
-        for (int l = 0; l < C; l++) res = res + t.v[C + 2 + l] * v[(cs + l) * kPad];  // :392-394
-      }
+      for (int l = 0; l < C; l++) sink(cs + l, t.v[C + 2 + l]);  // :392-394 / :210-212 / :417-421
     }
-    if (!HESS) s_out[(g * n + i) * kPad + lane] = res;
+    if (!HESS) o[i * kPad] = sink.res;
   }
   if (!HESS) {
     __syncthreads();
@@ -110,10 +162,11 @@ __global__ void __launch_bounds__(W * 32) hvp_reg_kernel(BatchArgs p) {
 }
 
 // ---------------------------------------------------------------- F3 Fletcher-Powell
-// params = [A (n*n) | B (n*n) | E* (n)].  AB_SMEM: (A_kj, B_kj) interleaved into shared memory
-// (n <= 32), else read from params through the read-only path.
-template <int KB, bool HESS, bool AB_SMEM>
+// params = [A (n*n) | B (n*n) | E* (n)].  AB_SMEM: (A_kj, B_kj) interleaved and transposed
+// into shared memory (n <= 32), else read from params through the read-only path.
+template <int KB, int MODE, bool AB_SMEM>
 __global__ void __launch_bounds__(kWarpsF3 * 32, 3) hvp_f3_kernel(BatchArgs p) {
+  constexpr bool HESS = mode_hess(MODE);
   extern __shared__ double smem[];
   const int n = p.n, G = p.groups, P = 32 * G, C = p.csize;
   double* s_sa = smem;                 // [G][n][33]  sin a
@@ -123,6 +176,8 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, 3) hvp_f3_kernel(BatchArgs p) {
   double2* s_ab = reinterpret_cast<double2*>(HESS ? s_vec : s_out + G * n * kPad);
   const int64_t e0 = (int64_t)blockIdx.x * P;
   stage_tile(p, e0, P, s_sa, HESS ? nullptr : s_vec);
+  if (MODE == MODE_SYM_HVP)
+    for (int q = threadIdx.x; q < G * n * kPad; q += blockDim.x) s_out[q] = 0.0;
   const double* A = p.params;
   const double* B = p.params + (size_t)n * n;
   if (AB_SMEM)
@@ -147,19 +202,21 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, 3) hvp_f3_kernel(BatchArgs p) {
   const double* sa = s_sa + g * n * kPad + lane;
   const double* ca = s_ca + g * n * kPad + lane;
   const double* v = HESS ? nullptr : s_vec + g * n * kPad + lane;
+  double* o = HESS ? nullptr : s_out + g * n * kPad + lane;
   const int64_t e = e0 + g * 32 + lane;
   const int nchunk = n / C;
   double R0[128], R1[128];
   for (int i = warp / G; i < n; i += rstep) {
-    double res = 0.0;
-    double* hrow = (HESS && e < p.m) ? p.out + (e * n + i) * n : nullptr;
-    for (int j = 0; j < nchunk; j++) {
+    const int scn = i / C;
+    RowSink<MODE> sink = make_sink<MODE>(p, i, e, v, o);
+    for (int j = mode_sym(MODE) ? scn : 0; j < nchunk; j++) {
+      sink.mirror = j > scn;
       if (AB_SMEM)
-        res = f3_eval<KB, HESS>(n, C, i, j * C, sa, ca, kPad, ABShared{s_ab, n}, Es, v, hrow, R0, R1, res);
+        f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ABShared{s_ab, n}, Es, R0, R1, sink);
       else
-        res = f3_eval<KB, HESS>(n, C, i, j * C, sa, ca, kPad, ABGlobal{A, B, n}, Es, v, hrow, R0, R1, res);
+        f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ABGlobal{A, B, n}, Es, R0, R1, sink);
     }
-    if (!HESS) s_out[(g * n + i) * kPad + lane] = res;
+    if (!HESS) o[i * kPad] = sink.res;
   }
   if (!HESS) {
     __syncthreads();

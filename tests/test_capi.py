@@ -70,7 +70,7 @@ def test_argument_errors(lib):
     assert _call(lib, 3, 1, 1, 10) == 3          # prodsum n < 2
     assert _call(lib, 9, 4, 1, 10) == 3          # unknown func
     assert _call(lib, 2, 4, 1, 10, params=None) == 3  # F3 without params
-    assert _call(lib, 0, 12, 3, 10) == 4         # C=3 not compiled for the register path
+    assert _call(lib, 0, 512, 1, 10) == 4        # n beyond the compiled set
     assert _call(lib, 0, 4, 1, 0, None, None, None) == 0  # m == 0: empty no-op, no CUDA call
     assert lib.chessfad_hessian_batch(0, 4, 3, 10, ctypes.c_void_p(1), ctypes.c_void_p(1), None, None) == 2
 
@@ -78,8 +78,10 @@ def test_argument_errors(lib):
 def test_is_supported(lib):
     import paper_2410_22575_b200 as chf
     assert chf.is_supported("rosenbrock", 16, 4)
-    assert not chf.is_supported("rosenbrock", 16, 3)
-    assert not chf.is_supported("rosenbrock", 12, 3)
+    assert not chf.is_supported("rosenbrock", 16, 3)   # 3 does not divide 16
+    assert chf.is_supported("rosenbrock", 12, 3)       # column groups of 1
+    assert chf.is_supported("rosenbrock", 128, 64)     # column groups of 16
+    assert not chf.is_supported("ackley", 256, 16)     # shared-memory budget
     assert chf.is_supported("fletcher_powell", 12, 3)  # runtime-C schedule
     assert chf.is_supported("fletcher_powell", 128, 8)
     assert not chf.is_supported("fletcher_powell", 256, 8)
@@ -110,3 +112,26 @@ def test_model_flops_survey_table():
     assert chf.model_flops_per_point("rosenbrock", 16, 16) == 150928
     assert chf.model_flops_per_point("ackley", 16, 4) == 100160
     assert chf.model_flops_per_point("fletcher_powell", 16, 2) == pytest.approx(878e3, rel=1e-3)
+
+
+@pytest.mark.parametrize("func", FUNCS)
+@pytest.mark.parametrize("n,C", [(4, 2), (8, 2), (6, 3), (8, 8)])
+def test_model_flops_symmetric_match_oracle_counts(func, n, C):
+    """Alg 8 / Alg 6 model (n(n/C+1)/2 evaluations; 2n^2 dot for Alg 8) ==
+    the oracle's counting build."""
+    import paper_2410_22575_b200 as chf
+    params = synth.fp_params_flat(0, n) if func == "fletcher_powell" else None
+    a = synth.points(0, n, 1)[0] + 3.0
+    _, c = oracle.count(oracle.sc_hess_vec, func, a, a, C, params)
+    assert chf.model_flops_per_point(func, n, C, algo="sym_hvp") == c["mul"] + c["add"]
+    _, c = oracle.count(oracle.hessian, func, a, params, algo="schunk", C=C)
+    assert chf.model_flops_per_point(func, n, C, algo="sym_hessian") == c["mul"] + c["add"]
+    assert chf.model_flops_per_point(func, n, C, algo="hvp") == chf.model_flops_per_point(func, n, C)
+
+
+def test_symmetric_support():
+    import paper_2410_22575_b200 as chf
+    for algo in ("hvp", "hessian", "sym_hvp", "sym_hessian"):
+        assert chf.is_supported("rosenbrock", 16, 4, algo)
+        assert chf.is_supported("fletcher_powell", 16, 4, algo)
+    assert not chf.is_supported("rosenbrock", 16, 3, "sym_hvp")

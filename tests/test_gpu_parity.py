@@ -68,7 +68,7 @@ def test_config1_every_point(chf):
 
 # ------------------------------------------------------------ sweep of n, C: several tiles + ragged tail
 @pytest.mark.parametrize("func", FUNCS)
-@pytest.mark.parametrize("n", [2, 3, 4, 8, 16, 32])
+@pytest.mark.parametrize("n", [2, 3, 4, 6, 8, 12, 16, 32])
 def test_parity_sweep(chf, func, n):
     m = 3 * 32 * 8 + 13  # several CTAs of the widest tile and a ragged tail
     if func == "fletcher_powell" and n >= 32:
@@ -89,7 +89,7 @@ def test_large_n(chf, func):
         P, V = synth.points(2, n, m), synth.vectors(2, n, m)
         params = _params(func, n)
         ref, sabs = oracle.hvp_batch(func, P, V, n if n <= 32 else 32, params)
-        for C in [1, 8, 32]:
+        for C in [1, 8, 32, 64, n]:
             if chf.is_supported(func, n, C):
                 _check(_gpu_hvp(chf, func, P, V, C, params), ref, sabs)
 
@@ -213,3 +213,61 @@ def test_full_size_sampled(chf, func):
     for C in (1, 4, 16):
         got = _gpu_hvp(chf, func, P, V, C, params)
         _check(got[idx], ref, sabs)
+
+
+# ------------------------------------------------------------ NEXT-1 / NEXT-2: symmetric algorithms
+@pytest.mark.parametrize("func", FUNCS)
+@pytest.mark.parametrize("n", [2, 6, 16, 32])
+def test_sym_hvp_parity(chf, func, n):
+    """Alg 8 on the GPU vs the oracle's Alg 8 (same accumulation order up to contraction) and
+    vs Alg 7 (the same product)."""
+    m = 300 if not (func == "fletcher_powell" and n == 32) else 120
+    P, V = synth.points(14, n, m), synth.vectors(14, n, m)
+    params = _params(func, n)
+    ref7, sabs = oracle.hvp_batch(func, P, V, 1, params)
+    dev = torch.device("cuda")
+    pr = None if params is None else torch.from_numpy(params).to(dev)
+    for C in divisors(n):
+        if not chf.is_supported(func, n, C, "sym_hvp"):
+            continue
+        got = chf.sym_hvp_batch(func, torch.from_numpy(P).to(dev), torch.from_numpy(V).to(dev), C, pr).cpu().numpy()
+        ref8 = oracle.sc_hvp_batch(func, P, V, C, params)
+        _check(got, ref8, sabs)
+        _check(got, ref7, sabs)
+
+
+@pytest.mark.parametrize("func", ["rosenbrock", "prodsum"])
+def test_sym_hvp_integer_bitwise(chf, func):
+    n, m = 16, 200
+    P, V = synth.int_points(15, n, m), synth.int_vectors(15, n, m)
+    want = np.zeros((m, n))
+    for e in range(m):
+        H = cf.rosenbrock_hessian_exact(P[e]) if func == "rosenbrock" else cf.prodsum_hessian_exact(n)
+        want[e] = [float(x) for x in cf.exact_hvp(H, V[e])]
+    for C in (1, 2, 4, 8, 16):
+        got = chf.sym_hvp_batch(func, torch.from_numpy(P).cuda(), torch.from_numpy(V).cuda(), C).cpu().numpy()
+        assert np.array_equal(got, want), C
+
+
+@pytest.mark.parametrize("func", FUNCS)
+def test_sym_hessian_parity(chf, func):
+    """Alg 6 on the GPU: equals the oracle's Alg 6 within rounding, its computed (upper-chunk)
+    entries equal the GPU's Alg 5 bit for bit, and it is exactly symmetric outside the
+    diagonal chunks."""
+    n, m = 16, 150
+    P = synth.points(16, n, m)
+    params = _params(func, n)
+    dev = torch.device("cuda")
+    pr = None if params is None else torch.from_numpy(params).to(dev)
+    pts = torch.from_numpy(P).to(dev)
+    for C in (1, 2, 4, 8, 16):
+        Hs = chf.sym_hessian_batch(func, pts, C, pr).cpu().numpy()
+        Hf = chf.hessian_batch(func, pts, C, pr).cpu().numpy()
+        ref = np.stack([oracle.hessian(func, P[e], params, algo="schunk", C=C)[0] for e in range(m)])
+        scale = np.abs(ref).reshape(m, -1).max(axis=1)
+        assert (np.abs(Hs - ref).reshape(m, -1).max(axis=1) / scale).max() <= TIGHT
+        blk = np.arange(n) // C
+        upper = blk[:, None] <= blk[None, :]
+        assert np.array_equal(Hs[:, upper], Hf[:, upper])
+        lower = blk[:, None] > blk[None, :]
+        assert np.array_equal(Hs[:, lower], Hs.transpose(0, 2, 1)[:, lower])
