@@ -24,24 +24,28 @@ def main():
     ap.add_argument("--funcs", nargs="*", default=["rosenbrock", "ackley", "fletcher_powell", "prodsum"])
     ap.add_argument("--csizes", nargs="*", type=int, default=[1, 2, 4, 8, 16])
     ap.add_argument("--hessian", action="store_true")
+    ap.add_argument("--algo", default=None, choices=list(chf.ALGOS))
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     n, m = args.n, args.m
     pts = torch.from_numpy(synth.points(0, n, m)).to(dev)
     vec = torch.from_numpy(synth.vectors(0, n, m)).to(dev)
     params = torch.from_numpy(synth.fp_params_flat(0, n)).to(dev)
+    algo = args.algo or ("hessian" if args.hessian else "hvp")
+    fn = {"hvp": chf.hvp_batch, "sym_hvp": chf.sym_hvp_batch, "hessian": chf.hessian_batch,
+          "sym_hessian": chf.sym_hessian_batch}[algo]
     for f in args.funcs:
         for c in args.csizes:
-            if n % c or not chf.is_supported(f, n, c):
+            if n % c or not chf.is_supported(f, n, c, algo):
                 continue
             pr = params if f == "fletcher_powell" else None
-            if args.hessian:
-                chf.hessian_batch(f, pts, c, pr)
+            if algo in ("hessian", "sym_hessian"):
+                fn(f, pts, c, pr)
             else:
-                chf.hvp_batch(f, pts, vec, c, pr)
+                fn(f, pts, vec, c, pr)
             torch.cuda.synchronize()
-            print(f"launch {f} n={n} C={c} m={m} flops_per_point={chf.model_flops_per_point(f, n, c, args.hessian):.0f}",
-                  flush=True)
+            print(f"launch {f} n={n} C={c} m={m} flops_per_point={chf.model_flops_per_point(f, n, c, algo=algo):.0f}"
+                  f" algo={algo}", flush=True)
 
 
 if __name__ == "__main__":

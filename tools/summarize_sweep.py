@@ -21,12 +21,13 @@ def load(csv_path, order_path):
     for lid, (k, v) in enumerate(sorted(per.items())):
         if lid >= len(order):
             break
-        _, func, n, C, m, fl = order[lid]
+        _, func, n, C, m, fl = order[lid][:6]
+        algo = order[lid][6].split("=")[1] if len(order[lid]) > 6 else "hvp"
         n, C, m = int(n[2:]), int(C[2:]), int(m[2:])
         model = float(fl.split("=")[1]) * m
         ex = 2 * v["sm__sass_thread_inst_executed_op_dfma_pred_on.sum"] + v["sm__sass_thread_inst_executed_op_dmul_pred_on.sum"] + v["sm__sass_thread_inst_executed_op_dadd_pred_on.sum"]
         t = v["gpu__time_duration.sum"] * 1e-9
-        out.append({"func": func, "n": n, "C": C, "m": m, "time_ms": t * 1e3,
+        out.append({"func": func, "n": n, "C": C, "m": m, "algo": algo, "time_ms": t * 1e3,
                     "model_flops": model, "executed_flops": ex, "executed_over_model": ex / model,
                     "fp64_warp_inst": v["sm__inst_executed_pipe_fp64.sum"],
                     "fp64_pipe_active_pct": v["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"],
@@ -54,7 +55,7 @@ def update_table(res, table_path):
     if tab.get("src_hash") != h:
         tab = {"src_hash": h, "entries": {}}
     for r in res:
-        key = f"{r['func']} n={r['n']} C={r['C']}"
+        key = f"{r['func']} n={r['n']} C={r['C']}" + ("" if r.get("algo", "hvp") == "hvp" else f" {r['algo']}")
         tab["entries"][key] = {"executed_flops_per_point": r["executed_flops"] / r["m"],
                                "model_flops_per_point": r["model_flops"] / r["m"],
                                "fp64_pipe_active_pct": r["fp64_pipe_active_pct"],
@@ -68,9 +69,9 @@ def update_table(res, table_path):
 
 if __name__ == "__main__":
     res = load(sys.argv[1], sys.argv[2])
-    print(f"{'func':16s} {'C':>3s} {'ms':>7s} {'exec/model':>10s} {'fp64pipe%':>9s} {'fl/inst':>7s} {'fp64share':>9s} {'DRAM MB':>8s} {'regs':>4s} {'warps%':>6s} {'GHz':>5s}")
+    print(f"{'func':16s} {'algo':11s} {'n':>3s} {'C':>3s} {'ms':>7s} {'exec/model':>10s} {'fp64pipe%':>9s} {'fl/inst':>7s} {'fp64share':>9s} {'DRAM MB':>8s} {'regs':>4s} {'warps%':>6s} {'GHz':>5s}")
     for r in res:
-        print(f"{r['func']:16s} {r['C']:3d} {r['time_ms']:7.2f} {r['executed_over_model']:10.3f} {r['fp64_pipe_active_pct']:9.1f} "
+        print(f"{r['func']:16s} {r['algo']:11s} {r['n']:3d} {r['C']:3d} {r['time_ms']:7.2f} {r['executed_over_model']:10.3f} {r['fp64_pipe_active_pct']:9.1f} "
               f"{r['executed_flop_per_fp64_lane_inst']:7.3f} {r['fp64_inst_share']:9.3f} {r['dram_bytes']/1e6:8.1f} {r['regs']:4.0f} "
               f"{r['warps_active_pct']:6.1f} {r['sm_clock_ghz']:5.2f}")
     if len(sys.argv) > 3:
