@@ -38,11 +38,10 @@ struct ABShared {
   int n;
   CHF_INL double2 get(int k, int j) const { return abT[j * n + k]; }
 };
-struct ABGlobal {
-  const double* A;
-  const double* B;
+struct ABGlobal {  // same interleaved, transposed layout in global scratch (n > 32)
+  const double2* abT;
   int n;
-  CHF_INL double2 get(int k, int j) const { return make_double2(__ldg(A + k * n + j), __ldg(B + k * n + j)); }
+  CHF_INL double2 get(int k, int j) const { return __ldg(abT + j * n + k); }
 };
 
 // accumulate variable j into KB k-rows of two slots:  Ep[kk] (+)= A_kj*sp + B_kj*cp, same for q

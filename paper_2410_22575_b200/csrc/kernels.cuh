@@ -75,7 +75,8 @@ CHF_INL void write_tile(const BatchArgs& p, int64_t e0, int P, const double* s_o
 template <int MODE>
 struct RowSink {
   double res;       // HVP modes: this row's accumulator
-  const double* v;  // lane's vector column (stride kPad), HVP modes
+  const double* v;  // lane's vector (stride vs), HVP modes
+  int vs;
   double* s_res;    // lane's output column (stride kPad), MODE_SYM_HVP scatter target
   double vi;        // v[i], MODE_SYM_HVP
   double* hrow;     // &H[e][i][0] (nullptr for ragged-tail lanes), Hessian modes
@@ -84,7 +85,7 @@ struct RowSink {
   bool mirror;      // symmetric modes: this chunk lies strictly after row i's chunk
   CHF_INL void operator()(int col, double h) {
     if (MODE == MODE_HVP || MODE == MODE_SYM_HVP) {
-      res = res + h * v[col * kPad];
+      res = res + h * v[col * vs];
       if (MODE == MODE_SYM_HVP && mirror) s_res[col * kPad] = s_res[col * kPad] + h * vi;
     } else if (hrow) {
       hrow[col] = h;
@@ -94,14 +95,15 @@ struct RowSink {
 };
 
 template <int MODE>
-CHF_INL RowSink<MODE> make_sink(const BatchArgs& p, int i, int64_t e, const double* v, double* o) {
+CHF_INL RowSink<MODE> make_sink(const BatchArgs& p, int i, int64_t e, const double* v, double* o, int vs = kPad) {
   constexpr bool HESS = mode_hess(MODE);
   const int n = p.n;
   RowSink<MODE> s;
   s.res = MODE == MODE_SYM_HVP ? o[i * kPad] : 0.0;
   s.v = v;
+  s.vs = vs;
   s.s_res = o;
-  s.vi = HESS ? 0.0 : v[i * kPad];
+  s.vi = HESS ? 0.0 : v[i * vs];
   s.hrow = (HESS && e < p.m) ? p.out + (e * n + i) * n : nullptr;
   s.hcol = (HESS && e < p.m) ? p.out + e * n * n + i : nullptr;
   s.n = n;
@@ -162,29 +164,41 @@ __global__ void __launch_bounds__(W * 32) hvp_reg_kernel(BatchArgs p) {
 }
 
 // ---------------------------------------------------------------- F3 Fletcher-Powell
-// params = [A (n*n) | B (n*n) | E* (n)].  AB_SMEM: (A_kj, B_kj) interleaved and transposed
-// into shared memory (n <= 32), else read from params through the read-only path.
-template <int KB, int MODE, bool AB_SMEM>
-__global__ void __launch_bounds__(kWarpsF3 * 32, 3) hvp_f3_kernel(BatchArgs p) {
+// params = [A (n*n) | B (n*n) | E* (n)].  (A_kj, B_kj) are interleaved and transposed,
+// abT[j*n + k], so that the KB k-values of one j are 16-byte broadcast loads at immediate
+// offsets: in shared memory when AB_SMEM (n <= 32), else in a global scratch copy built by
+// f3_ab_prep_kernel.  SLIM (n > 32): only sin/cos tiles in shared memory; vectors are read
+// and outputs written straight from/to global memory so that 3 CTAs fit per SM.
+static __global__ void f3_ab_prep_kernel(int n, const double* __restrict__ params, double2* __restrict__ abT) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n * n) return;
+  const int k = q / n, j = q - k * n;
+  abT[j * n + k] = make_double2(params[q], params[n * n + q]);
+}
+
+template <int KB, int MODE, bool AB_SMEM, bool SLIM>
+__global__ void __launch_bounds__(kWarpsF3 * 32, 3) hvp_f3_kernel(BatchArgs p, const double2* __restrict__ abT_g) {
   constexpr bool HESS = mode_hess(MODE);
+  constexpr bool VEC_TILE = !HESS && !SLIM;
   extern __shared__ double smem[];
   const int n = p.n, G = p.groups, P = 32 * G, C = p.csize;
   double* s_sa = smem;                 // [G][n][33]  sin a
   double* s_ca = s_sa + G * n * kPad;  // [G][n][33]  cos a
   double* s_vec = s_ca + G * n * kPad;
   double* s_out = s_vec + G * n * kPad;
-  double2* s_ab = reinterpret_cast<double2*>(HESS ? s_vec : s_out + G * n * kPad);
+  double2* s_ab = reinterpret_cast<double2*>(VEC_TILE ? s_out + G * n * kPad : s_vec);
   const int64_t e0 = (int64_t)blockIdx.x * P;
-  stage_tile(p, e0, P, s_sa, HESS ? nullptr : s_vec);
+  stage_tile(p, e0, P, s_sa, VEC_TILE ? s_vec : nullptr);
   if (MODE == MODE_SYM_HVP)
     for (int q = threadIdx.x; q < G * n * kPad; q += blockDim.x) s_out[q] = 0.0;
-  const double* A = p.params;
-  const double* B = p.params + (size_t)n * n;
-  if (AB_SMEM)
+  if (AB_SMEM) {
+    const double* A = p.params;
+    const double* B = p.params + (size_t)n * n;
     for (int q = threadIdx.x; q < n * n; q += blockDim.x) {
       const int k = q / n, j = q - k * n;
       s_ab[j * n + k] = make_double2(A[q], B[q]);  // transposed: [j][k]
     }
+  }
   __syncthreads();
   // g, g', g'' of the seeded inputs: sin a_k, cos a_k once per tile (see f3.cuh)
   for (int q = threadIdx.x; q < G * n * 32; q += blockDim.x) {
@@ -201,24 +215,32 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, 3) hvp_f3_kernel(BatchArgs p) {
   const int g = warp % G, rstep = kWarpsF3 / G;
   const double* sa = s_sa + g * n * kPad + lane;
   const double* ca = s_ca + g * n * kPad + lane;
-  const double* v = HESS ? nullptr : s_vec + g * n * kPad + lane;
-  double* o = HESS ? nullptr : s_out + g * n * kPad + lane;
   const int64_t e = e0 + g * 32 + lane;
+  const int64_t ec = e < p.m ? e : p.m - 1;
+  // vector column of this lane: shared tile (stride kPad) or global row (stride 1)
+  const double* v = HESS ? nullptr : (VEC_TILE ? s_vec + g * n * kPad + lane : p.vecs + ec * n);
+  double* o = (HESS || SLIM) ? nullptr : s_out + g * n * kPad + lane;
   const int nchunk = n / C;
   double R0[128], R1[128];
   for (int i = warp / G; i < n; i += rstep) {
     const int scn = i / C;
-    RowSink<MODE> sink = make_sink<MODE>(p, i, e, v, o);
+    RowSink<MODE> sink = make_sink<MODE>(p, i, e, v, o, VEC_TILE ? kPad : 1);
     for (int j = mode_sym(MODE) ? scn : 0; j < nchunk; j++) {
       sink.mirror = j > scn;
       if (AB_SMEM)
         f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ABShared{s_ab, n}, Es, R0, R1, sink);
       else
-        f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ABGlobal{A, B, n}, Es, R0, R1, sink);
+        f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ABGlobal{abT_g, n}, Es, R0, R1, sink);
     }
-    if (!HESS) o[i * kPad] = sink.res;
+    if (!HESS) {
+      if (SLIM) {
+        if (e < p.m) p.out[e * n + i] = sink.res;
+      } else {
+        o[i * kPad] = sink.res;
+      }
+    }
   }
-  if (!HESS) {
+  if (!HESS && !SLIM) {
     __syncthreads();
     write_tile(p, e0, P, s_out);
   }

@@ -24,19 +24,21 @@ inline size_t reg_smem_bytes(int func, int n, int G, int mode) {
 }
 
 inline bool f3_ab_smem(int n) { return n <= 32; }
+// slim tiles (no vector / output tiles) for n > 32; the symmetric HVP needs its output tile
+inline bool f3_slim(int n, int mode) { return n > 32 && mode != MODE_SYM_HVP; }
 
 inline size_t f3_smem_bytes(int n, int G, int mode) {
-  return (size_t)(mode_hess(mode) ? 2 : 4) * G * n * kPad * sizeof(double) +
-         (f3_ab_smem(n) ? (size_t)n * n * 2 * sizeof(double) : 0);
+  const int tiles = (mode_hess(mode) || f3_slim(n, mode)) ? 2 : 4;
+  return (size_t)tiles * G * n * kPad * sizeof(double) + (f3_ab_smem(n) ? (size_t)n * n * 2 * sizeof(double) : 0);
 }
 
-template <class K>
-inline cudaError_t launch_with_smem(K kernel, int grid, int block, size_t smem, cudaStream_t s, const BatchArgs& a) {
+template <class K, class... Args>
+inline cudaError_t launch_with_smem(K kernel, int grid, int block, size_t smem, cudaStream_t s, const Args&... args) {
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  kernel<<<grid, block, smem, s>>>(a);
+  kernel<<<grid, block, smem, s>>>(args...);
   return cudaGetLastError();
 }
 
@@ -49,13 +51,25 @@ cudaError_t launch_reg(BatchArgs a, cudaStream_t s) {
                           reg_smem_bytes(FUNC, a.n, a.groups, MODE), s, a);
 }
 
+// n > 32: (A, B) interleaved + transposed into stream-ordered scratch, freed on the stream
 template <int KB, int MODE, bool AB_SMEM>
 cudaError_t launch_f3(BatchArgs a, cudaStream_t s) {
   a.groups = groups_for(a.n, kWarpsF3, MODE);
   const int64_t P = 32 * a.groups;
   const int grid = (int)((a.m + P - 1) / P);
-  return launch_with_smem(hvp_f3_kernel<KB, MODE, AB_SMEM>, grid, kWarpsF3 * 32, f3_smem_bytes(a.n, a.groups, MODE),
-                          s, a);
+  const size_t smem = f3_smem_bytes(a.n, a.groups, MODE);
+  if (AB_SMEM) return launch_with_smem(hvp_f3_kernel<KB, MODE, true, false>, grid, kWarpsF3 * 32, smem, s, a,
+                                       (const double2*)nullptr);
+  double2* abT = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&abT, (size_t)a.n * a.n * sizeof(double2), s);
+  if (e != cudaSuccess) return e;
+  f3_ab_prep_kernel<<<(a.n * a.n + 255) / 256, 256, 0, s>>>(a.n, a.params, abT);
+  e = f3_slim(a.n, MODE)
+          ? launch_with_smem(hvp_f3_kernel<KB, MODE, false, true>, grid, kWarpsF3 * 32, smem, s, a, (const double2*)abT)
+          : launch_with_smem(hvp_f3_kernel<KB, MODE, false, false>, grid, kWarpsF3 * 32, smem, s, a,
+                             (const double2*)abT);
+  const cudaError_t e2 = cudaFreeAsync(abT, s);
+  return e != cudaSuccess ? e : e2;
 }
 
 // explicit-instantiation declarations (definitions in inst_*.cu)
