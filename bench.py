@@ -333,7 +333,7 @@ def main():
     if ex is not None:
         exec_tf = m * ex["executed_flops_per_point"] / per_step / 1e12
         traffic = ex["dram_bytes_per_launch"] * m / ex["m"]
-        accounting = ("executed FP64 FLOPs (2*DFMA+DMUL+DADD per point, ncu, this build) x m / event time; "
+        accounting = ("executed FP64 FLOPs (2*DFMA+DMUL+DADD per point; " + ex["basis"] + ") x m / event time; "
                       "model FLOPs reported as model_tflops_effective")
     else:
         exec_tf, traffic = None, None
@@ -379,14 +379,27 @@ def main():
     return 0
 
 
-def executed_entry(func, n, C, src_hash):
+def executed_entry(func, n, C, src_hash, algo="hvp"):
+    """ncu-measured executed FLOPs/point of this build (profiles/executed_flops.json).  If the
+    table was measured on an earlier build, its executed/model ratio is applied to this build's
+    model count and the entry is marked stale (its 'basis' field says so)."""
     try:
         tab = json.load(open(os.path.join(ROOT, "profiles", "executed_flops.json")))
     except Exception:
         return None
-    if tab.get("src_hash") != src_hash:
+    key = f"{func} n={n} C={C}" + ("" if algo == "hvp" else f" {algo}")
+    ent = tab.get("entries", {}).get(key)
+    if ent is None:
         return None
-    return tab.get("entries", {}).get(f"{func} n={n} C={C}")
+    ent = dict(ent)
+    if tab.get("src_hash") == src_hash:
+        ent["basis"] = f"ncu on this build ({src_hash})"
+    else:
+        import paper_2410_22575_b200 as chf
+        ratio = ent["executed_flops_per_point"] / ent["model_flops_per_point"]
+        ent["executed_flops_per_point"] = ratio * chf.model_flops_per_point(func, n, C, algo=algo)
+        ent["basis"] = f"STALE: executed/model ratio {ratio:.3f} measured by ncu on build {tab.get('src_hash')}"
+    return ent
 
 
 class _Null:
