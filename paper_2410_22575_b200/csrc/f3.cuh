@@ -9,10 +9,10 @@
 // beyond tiny n*C, so the evaluation DAG is executed in a different topological order
 // that needs O(KB) registers:
 //   phase A   slots 0 and 1 of every intermediate (they are shared by all columns);
-//             r_k slots 0/1 are kept in a per-thread array R0/R1.
 //   phase B   for each column c of the chunk: slots 2+c and C+2+c of every
 //             intermediate, which by slot independence need only slots
-//             {0, 1, 2+c, C+2+c} of their operands.
+//             {0, 1, 2+c, C+2+c} of their operands;
+//   both are blocked over KB residuals r_k at a time (see f3_eval).
 // Every scalar operation of the hDual evaluation is executed once (except g''*u1 of the
 // 2n unary ops, recomputed per column: 2 DMUL per j per column) in the paper's per-slot
 // form; only the order of independent operations changes.  The result slot 2+c (first
@@ -65,39 +65,42 @@ CHF_INL void f3_accum(const AB& ab, int kb, int j, double sp, double cp, double 
 // For each column l in ascending order, sink(cs + l, d2f/dx_i dx_{cs+l}) consumes the
 // second-order slot C+2+l (the chunk dot of Alg 7, the store of Alg 5, the scatter of Alg 8).
 // sa/ca: sin/cos of the lane's coordinates, element j at [j * stride]; Es: E*.
-// R0/R1: per-thread scratch (n doubles).
+// Loop order: k-blocks outer, columns inner.  For each block of KB residuals r_k, slots 0/1
+// (phase A) are formed once and kept in registers, then every column's slots 2+c / C+2+c of
+// those r_k are formed and their r*r contributions added to the column's f accumulator
+// FC[c] (per-thread scratch, C doubles) in ascending k -- the same summation order as a
+// column-outer schedule, with O(KB) live state instead of the 2n residual slots.
 template <int KB, class AB, class Sink>
 CHF_INL void f3_eval(int n, int C, int i, int cs, const double* __restrict__ sa,
                      const double* __restrict__ ca, int stride, const AB& ab,
-                     const double* __restrict__ Es, double* R0, double* R1, Sink&& sink) {
-  // ---------------- phase A: slots 0 and 1
+                     const double* __restrict__ Es, double* FC, Sink&& sink) {
   for (int kb = 0; kb < n; kb += KB) {
-    double E0[KB], E1[KB];
+    // ---------------- phase A: slots 0 and 1 of r_k, k in [kb, kb+KB)
+    double r0[KB], r1[KB];
     {
-      const double s0 = sa[0], c0 = ca[0];
-      const double y1 = (0 == i) ? 1.0 : 0.0;
-      // sin(y_0) = <sin a, cos a * y1, ...>;  cos(y_0) = <cos a, -sin a * y1, ...>
-      f3_accum<KB, true>(ab, kb, 0, s0, c0, c0 * y1, (-s0) * y1, E0, E1);
-    }
-    for (int j = 1; j < n; j++) {
-      const double s0 = sa[j * stride], c0 = ca[j * stride];
-      const double y1 = (j == i) ? 1.0 : 0.0;
-      f3_accum<KB, false>(ab, kb, j, s0, c0, c0 * y1, (-s0) * y1, E0, E1);
-    }
+      double E0[KB], E1[KB];
+      {
+        const double s0 = sa[0], c0 = ca[0];
+        const double y1 = (0 == i) ? 1.0 : 0.0;
+        // sin(y_0) = <sin a, cos a * y1, ...>;  cos(y_0) = <cos a, -sin a * y1, ...>
+        f3_accum<KB, true>(ab, kb, 0, s0, c0, c0 * y1, (-s0) * y1, E0, E1);
+      }
+      for (int j = 1; j < n; j++) {
+        const double s0 = sa[j * stride], c0 = ca[j * stride];
+        const double y1 = (j == i) ? 1.0 : 0.0;
+        f3_accum<KB, false>(ab, kb, j, s0, c0, c0 * y1, (-s0) * y1, E0, E1);
+      }
 #pragma unroll
-    for (int kk = 0; kk < KB; kk++) {
-      const int k = kb + kk;
-      R0[k] = Es[k] - E0[kk];  // r_k = E*_k - E_k (s+ on slot 0, negation elsewhere)
-      R1[k] = -E1[kk];
+      for (int kk = 0; kk < KB; kk++) {
+        r0[kk] = Es[kb + kk] - E0[kk];  // r_k = E*_k - E_k (s+ on slot 0, negation elsewhere)
+        r1[kk] = -E1[kk];
+      }
     }
-  }
-  // f slots 0/1 (f = sum_k r_k * r_k) are dead for the HVP and the Hessian.
+    // f slots 0/1 (f = sum_k r_k * r_k) are dead for the HVP and the Hessian.
 
-  // ---------------- phase B: one column at a time
-  for (int c = 0; c < C; c++) {
-    const int col = cs + c;
-    double fC = 0.0;
-    for (int kb = 0; kb < n; kb += KB) {
+    // ---------------- phase B: columns 2+c / C+2+c of the same r_k
+    for (int c = 0; c < C; c++) {
+      const int col = cs + c;
       double E2[KB], EC[KB];
       {
         const double s0 = sa[0], c0 = ca[0];
@@ -114,17 +117,18 @@ CHF_INL void f3_eval(int n, int C, int i, int cs, const double* __restrict__ sa,
         const double c2 = (-s0) * y2, cC = (-s0) * yC + ((-c0) * y1) * y2;
         f3_accum<KB, false>(ab, kb, j, s2, c2, sC, cC, E2, EC);
       }
+      double fC = kb == 0 ? 0.0 : FC[c];
 #pragma unroll
       for (int kk = 0; kk < KB; kk++) {
-        const int k = kb + kk;
-        const double r0 = R0[k], r1 = R1[k], r2 = -E2[kk], rC = -EC[kk];
+        const double r2 = -E2[kk], rC = -EC[kk];
         // (r*r)[C+2+c] = r0 rC + r1 r2 + r1 r2 + r0 rC   (Fig. 1 term order)
-        const double rrC = r0 * rC + r1 * r2 + r1 * r2 + r0 * rC;
-        fC = (k == 0) ? rrC : fC + rrC;
+        const double rrC = r0[kk] * rC + r1[kk] * r2 + r1[kk] * r2 + r0[kk] * rC;
+        fC = (kb + kk == 0) ? rrC : fC + rrC;
       }
+      FC[c] = fC;
     }
-    sink(col, fC);
   }
+  for (int c = 0; c < C; c++) sink(cs + c, FC[c]);
 }
 
 }  // namespace chessfad

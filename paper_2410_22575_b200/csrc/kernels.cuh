@@ -221,16 +221,16 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, 3) hvp_f3_kernel(BatchArgs p, c
   const double* v = HESS ? nullptr : (VEC_TILE ? s_vec + g * n * kPad + lane : p.vecs + ec * n);
   double* o = (HESS || SLIM) ? nullptr : s_out + g * n * kPad + lane;
   const int nchunk = n / C;
-  double R0[128], R1[128];
+  double FC[128];  // per-column f accumulators of one evaluation (C <= n <= 128 used)
   for (int i = warp / G; i < n; i += rstep) {
     const int scn = i / C;
     RowSink<MODE> sink = make_sink<MODE>(p, i, e, v, o, VEC_TILE ? kPad : 1);
     for (int j = mode_sym(MODE) ? scn : 0; j < nchunk; j++) {
       sink.mirror = j > scn;
       if (AB_SMEM)
-        f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ABShared{s_ab, n}, Es, R0, R1, sink);
+        f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ABShared{s_ab, n}, Es, FC, sink);
       else
-        f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ABGlobal{abT_g, n}, Es, R0, R1, sink);
+        f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ABGlobal{abT_g, n}, Es, FC, sink);
     }
     if (!HESS) {
       if (SLIM) {

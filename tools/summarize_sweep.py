@@ -13,8 +13,8 @@ def load(csv_path, order_path):
     ix = {h: i for i, h in enumerate(hdr)}
     per = {}
     for r in rows[1:]:
-        if len(r) < len(hdr):
-            continue
+        if len(r) < len(hdr) or "hvp_" not in r[ix["Kernel Name"]]:
+            continue  # only the batch kernels (not the F3 (A,B) prep kernel)
         lid = int(r[ix["ID"]])
         per.setdefault(lid, {})[r[ix["Metric Name"]]] = float(r[ix["Metric Value"]].replace(",", ""))
     out = []
