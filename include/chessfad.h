@@ -108,7 +108,7 @@ int chessfad_hvp_batch_host(int func, int n, int csize, int64_t m, const double 
 
 /* 1 if (func, n, csize) runs for both chessfad_hvp_batch and chessfad_hessian_batch, else 0
  * (argument errors also give 0).  Compiled set: Fletcher-
- * Powell any csize | n, n <= 128; the other functions n <= 256 (Ackley n <= 160), with one
+ * Powell any csize | n, n <= 32 or (n <= 128 and n % 8 == 0); the other functions n <= 256 (Ackley n <= 160), with one
  * hDual<csize> per evaluation for csize in {1,2,4,8,16,32} and, for any other csize | n, csize/c'
  * column groups of the largest c' in {1,2,4,8,16} dividing csize (bit-identical results by
  * slot independence; slots 0/1 recomputed per group). */

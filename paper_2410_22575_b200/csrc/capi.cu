@@ -57,8 +57,9 @@ constexpr size_t kSmemMax = 227 * 1024;
 
 int supported(int func, int n, int csize, int mode) {
   (void)csize;  // every C | n runs (F3: runtime C; register path: reg_kernel_chunk)
-  if (func == CHESSFAD_FLETCHER_POWELL)
-    return n <= kMaxNF3 && f3_smem_bytes(n, groups_for(n, kWarpsF3, mode), mode) <= kSmemMax;
+  if (func == CHESSFAD_FLETCHER_POWELL)  // n > 32 streams (A, B) in 8-column cp.async stages
+    return n <= kMaxNF3 && (n <= 32 || n % kF3RingJ == 0) &&
+           f3_smem_bytes(n, groups_for(n, kWarpsF3, mode), mode) <= kSmemMax;
   const int fn = func == CHESSFAD_ACKLEY ? FUNC_ACKLEY : FUNC_ROSENBROCK;
   return n <= kMaxNReg && reg_smem_bytes(fn, n, groups_for(n, kWarpsReg, mode), mode) <= kSmemMax;
 }

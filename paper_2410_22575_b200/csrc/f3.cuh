@@ -30,34 +30,93 @@
 
 namespace chessfad {
 
-// (A_kj, B_kj) sources: interleaved and transposed in shared memory, abT[j*n + k] (one
-// 16-byte broadcast load; the KB k-values of one j sit at immediate offsets), or the
-// caller's params in global memory (two 8-byte broadcast loads through the read-only path)
+// (A_kj, B_kj) sources: interleaved and transposed, abT[j*n + k], so that the KB k-values of
+// one j are 16-byte warp-uniform broadcast loads at immediate offsets.
+//   ABShared  the whole matrix in shared memory (n <= 32)
+//   ABRing    n > 32: streamed from the global scratch copy through a per-warp cp.async
+//             double buffer of JC j-values x KB k-values (hides the L1/L2 latency that the
+//             direct global loads expose: ncu long_scoreboard stalls, profiles/r01)
 struct ABShared {
   const double2* abT;
   int n;
   CHF_INL double2 get(int k, int j) const { return abT[j * n + k]; }
 };
-struct ABGlobal {  // same interleaved, transposed layout in global scratch (n > 32)
-  const double2* abT;
-  int n;
-  CHF_INL double2 get(int k, int j) const { return __ldg(abT + j * n + k); }
+
+CHF_INL void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem_src));
+}
+CHF_INL void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+CHF_INL void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int KB, int JC>
+struct ABRing {
+  double2* buf;         // this warp's ring: 2 stages x JC x KB
+  const double2* abT;   // global scratch, [j][k]
+  int n, lane;
+  CHF_INL void issue(int kb, int j0, int stage) const {
+    for (int q = lane; q < JC * KB; q += 32) {
+      const int jj = q / KB, kk = q - jj * KB;
+      cp_async16(buf + (stage * JC + jj) * KB + kk, abT + (size_t)(j0 + jj) * n + kb + kk);
+    }
+    cp_async_commit();
+  }
 };
 
-// accumulate variable j into KB k-rows of two slots:  Ep[kk] (+)= A_kj*sp + B_kj*cp, same for q
-template <int KB, bool FIRST, class AB>
-CHF_INL void f3_accum(const AB& ab, int kb, int j, double sp, double cp, double sq, double cq,
-                      double (&Ep)[KB], double (&Eq)[KB]) {
+// E (+)= sum_j A_kj * p_j + B_kj * q_j for KB k-rows and two slots; vals(j, sp, cp, sq, cq)
+// yields the slot values of sin y_j (s*) and cos y_j (c*).  The first j initialises.
+template <int KB, bool FIRST, class V>
+CHF_INL void f3_fma(const double2& c, int kk, const V& v, double (&Ep)[KB], double (&Eq)[KB]) {
+  if (FIRST) {
+    Ep[kk] = c.x * v.sp + c.y * v.cp;
+    Eq[kk] = c.x * v.sq + c.y * v.cq;
+  } else {
+    Ep[kk] = Ep[kk] + c.x * v.sp + c.y * v.cp;
+    Eq[kk] = Eq[kk] + c.x * v.sq + c.y * v.cq;
+  }
+}
+
+struct SlotVals {
+  double sp, cp, sq, cq;
+};
+
+template <int KB, class Vals>
+CHF_INL void f3_sum_j(const ABShared& ab, int n, int kb, const Vals& vals, double (&Ep)[KB], double (&Eq)[KB]) {
+  {
+    const SlotVals v = vals(0);
 #pragma unroll
-  for (int kk = 0; kk < KB; kk++) {
-    const double2 c = ab.get(kb + kk, j);
-    if (FIRST) {
-      Ep[kk] = c.x * sp + c.y * cp;
-      Eq[kk] = c.x * sq + c.y * cq;
-    } else {
-      Ep[kk] = Ep[kk] + c.x * sp + c.y * cp;
-      Eq[kk] = Eq[kk] + c.x * sq + c.y * cq;
+    for (int kk = 0; kk < KB; kk++) f3_fma<KB, true>(ab.get(kb + kk, 0), kk, v, Ep, Eq);
+  }
+  for (int j = 1; j < n; j++) {
+    const SlotVals v = vals(j);
+#pragma unroll
+    for (int kk = 0; kk < KB; kk++) f3_fma<KB, false>(ab.get(kb + kk, j), kk, v, Ep, Eq);
+  }
+}
+
+template <int KB, int JC, class Vals>
+CHF_INL void f3_sum_j(const ABRing<KB, JC>& ab, int n, int kb, const Vals& vals, double (&Ep)[KB], double (&Eq)[KB]) {
+  const int nch = n / JC;  // n % JC == 0 on this path
+  ab.issue(kb, 0, 0);
+  for (int jc = 0; jc < nch; jc++) {
+    if (jc + 1 < nch) ab.issue(kb, (jc + 1) * JC, (jc + 1) & 1);
+    else cp_async_commit();  // empty group keeps wait_group<1> uniform
+    cp_async_wait<1>();
+    __syncwarp();
+    const double2* st = ab.buf + (jc & 1) * JC * KB;
+    if (jc == 0) {
+      const SlotVals v = vals(0);
+#pragma unroll
+      for (int kk = 0; kk < KB; kk++) f3_fma<KB, true>(st[kk], kk, v, Ep, Eq);
     }
+#pragma unroll 1
+    for (int jj = (jc == 0 ? 1 : 0); jj < JC; jj++) {
+      const SlotVals v = vals(jc * JC + jj);
+#pragma unroll
+      for (int kk = 0; kk < KB; kk++) f3_fma<KB, false>(st[jj * KB + kk], kk, v, Ep, Eq);
+    }
+    __syncwarp();  // the stage is refilled two chunks later
   }
 }
 
@@ -65,70 +124,54 @@ CHF_INL void f3_accum(const AB& ab, int kb, int j, double sp, double cp, double 
 // For each column l in ascending order, sink(cs + l, d2f/dx_i dx_{cs+l}) consumes the
 // second-order slot C+2+l (the chunk dot of Alg 7, the store of Alg 5, the scatter of Alg 8).
 // sa/ca: sin/cos of the lane's coordinates, element j at [j * stride]; Es: E*.
-// Loop order: k-blocks outer, columns inner.  For each block of KB residuals r_k, slots 0/1
-// (phase A) are formed once and kept in registers, then every column's slots 2+c / C+2+c of
-// those r_k are formed and their r*r contributions added to the column's f accumulator
-// FC[c] (per-thread scratch, C doubles) in ascending k -- the same summation order as a
-// column-outer schedule, with O(KB) live state instead of the 2n residual slots.
+// R0/R1: per-thread scratch (n doubles).
 template <int KB, class AB, class Sink>
 CHF_INL void f3_eval(int n, int C, int i, int cs, const double* __restrict__ sa,
                      const double* __restrict__ ca, int stride, const AB& ab,
-                     const double* __restrict__ Es, double* FC, Sink&& sink) {
+                     const double* __restrict__ Es, double* R0, double* R1, Sink&& sink) {
+  // ---------------- phase A: slots 0 and 1
+  // sin(y_j) = <sin a, cos a * y1, ...>;  cos(y_j) = <cos a, -sin a * y1, ...>
+  auto valsA = [&](int j) {
+    const double s0 = sa[j * stride], c0 = ca[j * stride];
+    const double y1 = (j == i) ? 1.0 : 0.0;
+    return SlotVals{s0, c0, c0 * y1, (-s0) * y1};
+  };
   for (int kb = 0; kb < n; kb += KB) {
-    // ---------------- phase A: slots 0 and 1 of r_k, k in [kb, kb+KB)
-    double r0[KB], r1[KB];
-    {
-      double E0[KB], E1[KB];
-      {
-        const double s0 = sa[0], c0 = ca[0];
-        const double y1 = (0 == i) ? 1.0 : 0.0;
-        // sin(y_0) = <sin a, cos a * y1, ...>;  cos(y_0) = <cos a, -sin a * y1, ...>
-        f3_accum<KB, true>(ab, kb, 0, s0, c0, c0 * y1, (-s0) * y1, E0, E1);
-      }
-      for (int j = 1; j < n; j++) {
-        const double s0 = sa[j * stride], c0 = ca[j * stride];
-        const double y1 = (j == i) ? 1.0 : 0.0;
-        f3_accum<KB, false>(ab, kb, j, s0, c0, c0 * y1, (-s0) * y1, E0, E1);
-      }
+    double E0[KB], E1[KB];
+    f3_sum_j<KB>(ab, n, kb, valsA, E0, E1);
 #pragma unroll
-      for (int kk = 0; kk < KB; kk++) {
-        r0[kk] = Es[kb + kk] - E0[kk];  // r_k = E*_k - E_k (s+ on slot 0, negation elsewhere)
-        r1[kk] = -E1[kk];
-      }
-    }
-    // f slots 0/1 (f = sum_k r_k * r_k) are dead for the HVP and the Hessian.
-
-    // ---------------- phase B: columns 2+c / C+2+c of the same r_k
-    for (int c = 0; c < C; c++) {
-      const int col = cs + c;
-      double E2[KB], EC[KB];
-      {
-        const double s0 = sa[0], c0 = ca[0];
-        const double y1 = (0 == i) ? 1.0 : 0.0, y2 = (0 == col) ? 1.0 : 0.0, yC = 0.0;
-        // sin: g' = cos a, g'' = -sin a;   cos: g' = -sin a, g'' = -cos a
-        const double s2 = c0 * y2, sC = c0 * yC + ((-s0) * y1) * y2;
-        const double c2 = (-s0) * y2, cC = (-s0) * yC + ((-c0) * y1) * y2;
-        f3_accum<KB, true>(ab, kb, 0, s2, c2, sC, cC, E2, EC);
-      }
-      for (int j = 1; j < n; j++) {
-        const double s0 = sa[j * stride], c0 = ca[j * stride];
-        const double y1 = (j == i) ? 1.0 : 0.0, y2 = (j == col) ? 1.0 : 0.0, yC = 0.0;
-        const double s2 = c0 * y2, sC = c0 * yC + ((-s0) * y1) * y2;
-        const double c2 = (-s0) * y2, cC = (-s0) * yC + ((-c0) * y1) * y2;
-        f3_accum<KB, false>(ab, kb, j, s2, c2, sC, cC, E2, EC);
-      }
-      double fC = kb == 0 ? 0.0 : FC[c];
-#pragma unroll
-      for (int kk = 0; kk < KB; kk++) {
-        const double r2 = -E2[kk], rC = -EC[kk];
-        // (r*r)[C+2+c] = r0 rC + r1 r2 + r1 r2 + r0 rC   (Fig. 1 term order)
-        const double rrC = r0[kk] * rC + r1[kk] * r2 + r1[kk] * r2 + r0[kk] * rC;
-        fC = (kb + kk == 0) ? rrC : fC + rrC;
-      }
-      FC[c] = fC;
+    for (int kk = 0; kk < KB; kk++) {
+      const int k = kb + kk;
+      R0[k] = Es[k] - E0[kk];  // r_k = E*_k - E_k (s+ on slot 0, negation elsewhere)
+      R1[k] = -E1[kk];
     }
   }
-  for (int c = 0; c < C; c++) sink(cs + c, FC[c]);
+  // f slots 0/1 (f = sum_k r_k * r_k) are dead for the HVP and the Hessian.
+
+  // ---------------- phase B: one column at a time
+  for (int c = 0; c < C; c++) {
+    const int col = cs + c;
+    // sin: g' = cos a, g'' = -sin a;   cos: g' = -sin a, g'' = -cos a
+    auto valsB = [&](int j) {
+      const double s0 = sa[j * stride], c0 = ca[j * stride];
+      const double y1 = (j == i) ? 1.0 : 0.0, y2 = (j == col) ? 1.0 : 0.0, yC = 0.0;
+      return SlotVals{c0 * y2, (-s0) * y2, c0 * yC + ((-s0) * y1) * y2, (-s0) * yC + ((-c0) * y1) * y2};
+    };
+    double fC = 0.0;
+    for (int kb = 0; kb < n; kb += KB) {
+      double E2[KB], EC[KB];
+      f3_sum_j<KB>(ab, n, kb, valsB, E2, EC);
+#pragma unroll
+      for (int kk = 0; kk < KB; kk++) {
+        const int k = kb + kk;
+        const double r0 = R0[k], r1 = R1[k], r2 = -E2[kk], rC = -EC[kk];
+        // (r*r)[C+2+c] = r0 rC + r1 r2 + r1 r2 + r0 rC   (Fig. 1 term order)
+        const double rrC = r0 * rC + r1 * r2 + r1 * r2 + r0 * rC;
+        fC = (k == 0) ? rrC : fC + rrC;
+      }
+    }
+    sink(col, fC);
+  }
 }
 
 }  // namespace chessfad

@@ -176,6 +176,8 @@ static __global__ void f3_ab_prep_kernel(int n, const double* __restrict__ param
   abT[j * n + k] = make_double2(params[q], params[n * n + q]);
 }
 
+constexpr int kF3RingJ = 8;  // j-values per cp.async stage of the (A, B) ring (n > 32)
+
 template <int KB, int MODE, bool AB_SMEM, bool SLIM>
 __global__ void __launch_bounds__(kWarpsF3 * 32, 3) hvp_f3_kernel(BatchArgs p, const double2* __restrict__ abT_g) {
   constexpr bool HESS = mode_hess(MODE);
@@ -186,7 +188,8 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, 3) hvp_f3_kernel(BatchArgs p, c
   double* s_ca = s_sa + G * n * kPad;  // [G][n][33]  cos a
   double* s_vec = s_ca + G * n * kPad;
   double* s_out = s_vec + G * n * kPad;
-  double2* s_ab = reinterpret_cast<double2*>(VEC_TILE ? s_out + G * n * kPad : s_vec);
+  // (A, B): the whole matrix (AB_SMEM) or this CTA's per-warp cp.async rings
+  double2* s_ab = reinterpret_cast<double2*>((VEC_TILE || MODE == MODE_SYM_HVP) ? s_out + G * n * kPad : s_vec);
   const int64_t e0 = (int64_t)blockIdx.x * P;
   stage_tile(p, e0, P, s_sa, VEC_TILE ? s_vec : nullptr);
   if (MODE == MODE_SYM_HVP)
@@ -221,16 +224,17 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, 3) hvp_f3_kernel(BatchArgs p, c
   const double* v = HESS ? nullptr : (VEC_TILE ? s_vec + g * n * kPad + lane : p.vecs + ec * n);
   double* o = (HESS || SLIM) ? nullptr : s_out + g * n * kPad + lane;
   const int nchunk = n / C;
-  double FC[128];  // per-column f accumulators of one evaluation (C <= n <= 128 used)
+  const ABRing<KB, kF3RingJ> ring{s_ab + warp * 2 * kF3RingJ * KB, abT_g, n, lane};
+  double R0[128], R1[128];  // per-thread residual slots 0/1 of one evaluation (n <= 128 used)
   for (int i = warp / G; i < n; i += rstep) {
     const int scn = i / C;
     RowSink<MODE> sink = make_sink<MODE>(p, i, e, v, o, VEC_TILE ? kPad : 1);
     for (int j = mode_sym(MODE) ? scn : 0; j < nchunk; j++) {
       sink.mirror = j > scn;
       if (AB_SMEM)
-        f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ABShared{s_ab, n}, Es, FC, sink);
+        f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ABShared{s_ab, n}, Es, R0, R1, sink);
       else
-        f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ABGlobal{abT_g, n}, Es, FC, sink);
+        f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ring, Es, R0, R1, sink);
     }
     if (!HESS) {
       if (SLIM) {

@@ -29,7 +29,9 @@ inline bool f3_slim(int n, int mode) { return n > 32 && mode != MODE_SYM_HVP; }
 
 inline size_t f3_smem_bytes(int n, int G, int mode) {
   const int tiles = (mode_hess(mode) || f3_slim(n, mode)) ? 2 : 4;
-  return (size_t)tiles * G * n * kPad * sizeof(double) + (f3_ab_smem(n) ? (size_t)n * n * 2 * sizeof(double) : 0);
+  const size_t ab = f3_ab_smem(n) ? (size_t)n * n * 2 * sizeof(double)                        // whole (A, B)
+                                  : (size_t)kWarpsF3 * 2 * kF3RingJ * 16 * 2 * sizeof(double);  // rings (KB <= 16)
+  return (size_t)tiles * G * n * kPad * sizeof(double) + ab;
 }
 
 template <class K, class... Args>
