@@ -178,8 +178,11 @@ static __global__ void f3_ab_prep_kernel(int n, const double* __restrict__ param
 
 constexpr int kF3RingJ = 8;  // j-values per cp.async stage of the (A, B) ring (n > 32)
 
+// min CTAs/SM: 3 (<= 168 registers) with (A, B) in shared memory; 2 (<= 255) for the ring
+// path, whose 16 broadcast loads per j need registers to be batched ahead of their DFMAs
 template <int KB, int MODE, bool AB_SMEM, bool SLIM>
-__global__ void __launch_bounds__(kWarpsF3 * 32, 3) hvp_f3_kernel(BatchArgs p, const double2* __restrict__ abT_g) {
+__global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? 3 : 2)
+    hvp_f3_kernel(BatchArgs p, const double2* __restrict__ abT_g) {
   constexpr bool HESS = mode_hess(MODE);
   constexpr bool VEC_TILE = !HESS && !SLIM;
   extern __shared__ double smem[];
