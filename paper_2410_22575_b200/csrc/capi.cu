@@ -60,8 +60,7 @@ int supported(int func, int n, int csize, int mode) {
   if (func == CHESSFAD_FLETCHER_POWELL)  // n > 32 streams (A, B) in 8-column cp.async stages
     return n <= kMaxNF3 && (n <= 32 || n % kF3RingJ == 0) &&
            f3_smem_bytes(n, groups_for(n, kWarpsF3, mode), mode) <= kSmemMax;
-  const int fn = func == CHESSFAD_ACKLEY ? FUNC_ACKLEY : FUNC_ROSENBROCK;
-  return n <= kMaxNReg && reg_smem_bytes(fn, n, groups_for(n, kWarpsReg, mode), mode) <= kSmemMax;
+  return n <= kMaxNReg && reg_smem_bytes(func == CHESSFAD_ACKLEY, n, groups_for(n, kWarpsReg, mode), mode) <= kSmemMax;
 }
 
 // largest power of two <= 16 that divides n: the F3 k-block

@@ -112,21 +112,22 @@ CHF_INL RowSink<MODE> make_sink(const BatchArgs& p, int i, int64_t e, const doub
 }
 
 // ---------------------------------------------------------------- F1, F2, F4: hDual<C> in registers
-template <int FUNC, int C, int MODE, int W>
-__global__ void __launch_bounds__(W * 32) hvp_reg_kernel(BatchArgs p) {
+template <class F, int C, int MODE, int W>
+__global__ void __launch_bounds__(W * 32) hvp_reg_kernel(BatchArgs p, F f) {
+  constexpr bool TRIG = uses_trig2pi<F>::value;
   constexpr bool HESS = mode_hess(MODE);
   extern __shared__ double smem[];
   const int n = p.n, G = p.groups, P = 32 * G, Capi = p.csize;
   double* s_pts = smem;
   double* s_vec = HESS ? nullptr : s_pts + G * n * kPad;
   double* s_out = HESS ? nullptr : s_vec + G * n * kPad;
-  double* s_sin = (HESS ? s_pts : s_out) + G * n * kPad;  // Ackley only
+  double* s_sin = (HESS ? s_pts : s_out) + G * n * kPad;  // TRIG only
   double* s_cos = s_sin + G * n * kPad;
   const int64_t e0 = (int64_t)blockIdx.x * P;
   stage_tile(p, e0, P, s_pts, s_vec);
   if (MODE == MODE_SYM_HVP)
     for (int q = threadIdx.x; q < G * n * kPad; q += blockDim.x) s_out[q] = 0.0;
-  if (FUNC == FUNC_ACKLEY) {
+  if (TRIG) {
     __syncthreads();
     for (int q = threadIdx.x; q < G * n * 32; q += blockDim.x) {
       const int idx = (q >> 5) * kPad + (q & 31);
@@ -140,8 +141,8 @@ __global__ void __launch_bounds__(W * 32) hvp_reg_kernel(BatchArgs p) {
   const double* a = s_pts + g * n * kPad + lane;
   const double* v = HESS ? nullptr : s_vec + g * n * kPad + lane;
   double* o = HESS ? nullptr : s_out + g * n * kPad + lane;
-  const double* tsin = FUNC == FUNC_ACKLEY ? s_sin + g * n * kPad + lane : nullptr;
-  const double* tcos = FUNC == FUNC_ACKLEY ? s_cos + g * n * kPad + lane : nullptr;
+  const double* tsin = TRIG ? s_sin + g * n * kPad + lane : nullptr;
+  const double* tcos = TRIG ? s_cos + g * n * kPad + lane : nullptr;
   const int64_t e = e0 + g * 32 + lane;
   const int nchunk = n / C;
   for (int i = warp / G; i < n; i += rstep) {
@@ -151,7 +152,7 @@ __global__ void __launch_bounds__(W * 32) hvp_reg_kernel(BatchArgs p) {
       const int cs = j * C;
       sink.mirror = cs / Capi > scn;
       const LaneSeed<C> y{a, kPad, i, cs, tsin, tcos};
-      const hd<C> t = eval_f<FUNC, C>(n, y);  // CHUNK-INIT + f<hDual<C>>, Alg 7 :389-390
+      const hd<C> t = f.template operator()<C>(n, y);  // CHUNK-INIT + f<hDual<C>>, Alg 7 :389-390
 #pragma unroll
       for (int l = 0; l < C; l++) sink(cs + l, t.v[C + 2 + l]);  // :392-394 / :210-212 / :417-421
     }

@@ -18,8 +18,8 @@ inline int groups_for(int n, int warps, int mode) {
   return g;
 }
 
-inline size_t reg_smem_bytes(int func, int n, int G, int mode) {
-  const int tiles = (mode_hess(mode) ? 1 : 3) + (func == FUNC_ACKLEY ? 2 : 0);
+inline size_t reg_smem_bytes(bool trig, int n, int G, int mode) {
+  const int tiles = (mode_hess(mode) ? 1 : 3) + (trig ? 2 : 0);
   return (size_t)tiles * G * n * kPad * sizeof(double);
 }
 
@@ -44,13 +44,19 @@ inline cudaError_t launch_with_smem(K kernel, int grid, int block, size_t smem, 
   return cudaGetLastError();
 }
 
-template <int FUNC, int C, int MODE>
-cudaError_t launch_reg(BatchArgs a, cudaStream_t s) {
+// any functor F (built-in or user, see testfuncs.cuh), hDual<C> in registers
+template <class F, int C, int MODE>
+cudaError_t launch_functor(const F& f, BatchArgs a, cudaStream_t s) {
   a.groups = groups_for(a.n, kWarpsReg, MODE);
   const int64_t P = 32 * a.groups;
   const int grid = (int)((a.m + P - 1) / P);
-  return launch_with_smem(hvp_reg_kernel<FUNC, C, MODE, kWarpsReg>, grid, kWarpsReg * 32,
-                          reg_smem_bytes(FUNC, a.n, a.groups, MODE), s, a);
+  return launch_with_smem(hvp_reg_kernel<F, C, MODE, kWarpsReg>, grid, kWarpsReg * 32,
+                          reg_smem_bytes(uses_trig2pi<F>::value, a.n, a.groups, MODE), s, a, f);
+}
+
+template <int FUNC, int C, int MODE>
+cudaError_t launch_reg(BatchArgs a, cudaStream_t s) {
+  return launch_functor<BuiltinFunc<FUNC>, C, MODE>(BuiltinFunc<FUNC>{}, a, s);
 }
 
 // n > 32: (A, B) interleaved + transposed into stream-ordered scratch, freed on the stream

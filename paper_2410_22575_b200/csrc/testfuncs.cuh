@@ -108,4 +108,28 @@ CHF_INL hd<C> eval_f(int n, const Seed& y) {
   else return f_prodsum<C>(n, y);
 }
 
+// The register-path kernel evaluates a FUNCTOR: any type with
+//     template <int C, class Seed> __device__ hd<C> operator()(int n, const Seed& y) const
+// where y(k) is the CHUNK-INIT seed hDual<C> of variable k.  The built-in test functions are
+// functors too; user functions (NEXT-3, "templated function on the data type")
+// plug into the same kernels through include/chessfad_device.cuh.
+// kTrig2Pi: the built-in Ackley tabulates sincos(2 pi a_k) per tile (Seed::sin2pi/cos2pi).
+template <int FUNC>
+struct BuiltinFunc {
+  static constexpr bool kTrig2Pi = FUNC == FUNC_ACKLEY;
+  template <int C, class Seed>
+  CHF_INL hd<C> operator()(int n, const Seed& y) const {
+    return eval_f<FUNC, C>(n, y);
+  }
+};
+
+template <class F, class = void>
+struct uses_trig2pi {
+  static constexpr bool value = false;
+};
+template <class F>
+struct uses_trig2pi<F, decltype((void)F::kTrig2Pi)> {
+  static constexpr bool value = F::kTrig2Pi;
+};
+
 }  // namespace chessfad
