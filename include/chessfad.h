@@ -98,13 +98,20 @@ int chessfad_sym_hessian_batch(int func, int n, int csize, int64_t m, const doub
  * End-to-end variant of chessfad_hvp_batch on HOST buffers: points, vecs, out (m x n) and
  * params are HOST pointers (pinned memory gives copy/compute overlap; pageable memory
  * works but serialises).  The batch is split into pieces of `piece_points` points
- * (<= 0: library default) that flow H2D -> kernel -> D2H through two CUDA streams so
- * that copies overlap computation.  Device scratch is allocated stream-ordered and freed
- * before return.  SYNCHRONOUS: returns after `out` holds the result.  `stream` orders the
- * work after prior work on it (NULL = legacy default stream).
+ * (<= 0: library default, m/16) flowing through a three-stage pipeline -- an H2D stream,
+ * a compute stream and a D2H stream with three device buffer sets -- so that both copy
+ * directions overlap the kernels.  Device scratch: `workspace` (DEVICE, at least
+ * chessfad_hvp_host_workspace_bytes(...) bytes, owned by the caller), or NULL to allocate
+ * stream-ordered scratch inside the call.  SYNCHRONOUS: returns after `out` holds the
+ * result.  `stream` orders the work after prior work on it (NULL = legacy default stream).
+ * ERR_ARG if the workspace is too small.
  */
 int chessfad_hvp_batch_host(int func, int n, int csize, int64_t m, const double *points, const double *vecs,
-                            double *out, const double *params, int64_t piece_points, void *stream);
+                            double *out, const double *params, int64_t piece_points, void *workspace,
+                            size_t workspace_bytes, void *stream);
+
+/* Device workspace bytes chessfad_hvp_batch_host needs for (func, n, m, piece_points). */
+size_t chessfad_hvp_host_workspace_bytes(int func, int n, int64_t m, int64_t piece_points);
 
 /* 1 if (func, n, csize) runs for both chessfad_hvp_batch and chessfad_hessian_batch, else 0
  * (argument errors also give 0).  Compiled set: Fletcher-

@@ -22,7 +22,7 @@ ALGOS = {"hvp": 0, "hessian": 1, "sym_hvp": 2, "sym_hessian": 3}
 EXPORTS = sorted(["chessfad_hvp_batch", "chessfad_hessian_batch", "chessfad_sym_hvp_batch", "chessfad_sym_hessian_batch",
                   "chessfad_hvp_batch_host", "chessfad_is_supported", "chessfad_is_supported_algo",
                   "chessfad_status_string", "chessfad_model_flops_per_point", "chessfad_model_flops_per_point_algo",
-                  "chessfad_fp64_probe", "chessfad_version"])
+                  "chessfad_fp64_probe", "chessfad_version", "chessfad_hvp_host_workspace_bytes"])
 
 _lock = threading.Lock()
 _lib = None
@@ -54,7 +54,8 @@ def load(build_if_missing: bool = True):
             "chessfad_sym_hessian_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_is_supported_algo": (i32, [i32, i32, i32, i32]),
             "chessfad_model_flops_per_point_algo": (dbl, [i32, i32, i32, i32]),
-            "chessfad_hvp_batch_host": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, i64, vp]),
+            "chessfad_hvp_batch_host": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, i64, vp, ctypes.c_size_t, vp]),
+            "chessfad_hvp_host_workspace_bytes": (ctypes.c_size_t, [i32, i32, i64, i64]),
             "chessfad_is_supported": (i32, [i32, i32, i32]),
             "chessfad_status_string": (ctypes.c_char_p, [i32]),
             "chessfad_model_flops_per_point": (dbl, [i32, i32, i32, i32]),
@@ -155,9 +156,11 @@ def _host_ptr(x, name, writable=False):
     return ctypes.c_void_p(a.ctypes.data), a
 
 
-def hvp_batch_host(func, points, vecs, csize: int, params=None, out=None, piece_points: int = 0, stream=None):
-    """End-to-end HVP on HOST buffers (numpy arrays or CPU tensors, ideally pinned):
-    H2D copies, kernels and D2H copies pipelined over two streams; synchronous."""
+def hvp_batch_host(func, points, vecs, csize: int, params=None, out=None, piece_points: int = 0, stream=None,
+                   workspace=None):
+    """End-to-end HVP on HOST buffers (numpy arrays or CPU tensors, ideally pinned): H2D
+    copies, kernels and D2H copies in a three-stage stream pipeline; synchronous.  The device
+    workspace comes from torch's caching allocator (or `workspace`, a CUDA uint8 tensor)."""
     import torch
     m, n = points.shape
     if out is None:
@@ -166,7 +169,12 @@ def hvp_batch_host(func, points, vecs, csize: int, params=None, out=None, piece_
     pv, _ = _host_ptr(vecs, "vecs")
     po, _ = _host_ptr(out, "out", writable=True)
     ppar, _ = _host_ptr(params, "params")
-    st = load().chessfad_hvp_batch_host(_func(func), n, csize, m, pp, pv, po, ppar, piece_points, _stream_ptr(stream))
+    lib = load()
+    need = lib.chessfad_hvp_host_workspace_bytes(_func(func), n, m, piece_points)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device="cuda")
+    st = lib.chessfad_hvp_batch_host(_func(func), n, csize, m, pp, pv, po, ppar, piece_points,
+                                     ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _stream_ptr(stream))
     _check(st)
     return out
 

@@ -166,66 +166,93 @@ int chessfad_sym_hessian_batch(int func, int n, int csize, int64_t m, const doub
   return batch_entry<MODE_SYM_HESS>(func, n, csize, m, points, nullptr, hess, params, stream);
 }
 
+namespace {
+constexpr int kHostSets = 3;  // buffer sets of the host pipeline (pieces in flight)
+int64_t host_piece(int64_t m, int64_t piece_points) {
+  if (piece_points <= 0) piece_points = std::max<int64_t>(4096, (m + 15) / 16);
+  return std::max<int64_t>(1, std::min(piece_points, m));
+}
+size_t host_ws_bytes(int func, int n, int64_t m, int64_t piece_points) {
+  const size_t pbytes = (size_t)host_piece(m, piece_points) * n * sizeof(double);
+  const size_t nparams = (func == CHESSFAD_FLETCHER_POWELL) ? (size_t)2 * n * n + n : 0;
+  return (size_t)kHostSets * 3 * pbytes + nparams * sizeof(double) + 256;
+}
+}  // namespace
+
+size_t chessfad_hvp_host_workspace_bytes(int func, int n, int64_t m, int64_t piece_points) {
+  if (n < 1 || m < 0) return 0;
+  return host_ws_bytes(func, n, m, piece_points);
+}
+
+// Three-stage pipeline over pieces of the batch: an H2D stream copies piece p into buffer set
+// p % 3 (after that set's previous D2H), a compute stream runs the kernel, a D2H stream copies
+// the result back -- the H2D copy engine never waits for a kernel, H2D and D2H overlap.
 int chessfad_hvp_batch_host(int func, int n, int csize, int64_t m, const double* points, const double* vecs,
-                            double* out, const double* params, int64_t piece_points, void* stream) {
+                            double* out, const double* params, int64_t piece_points, void* workspace,
+                            size_t workspace_bytes, void* stream) {
   int st = validate(func, n, csize, m, false, params, points, vecs, out);
   if (st) return st;
   if (!supported(func, n, csize, MODE_HVP)) return CHESSFAD_ERR_UNSUPPORTED;
   if (m == 0) return CHESSFAD_OK;
+  const size_t need = host_ws_bytes(func, n, m, piece_points);
+  if (workspace && workspace_bytes < need) return CHESSFAD_ERR_ARG;
   cudaStream_t s0 = (cudaStream_t)stream;
-  if (piece_points <= 0) piece_points = std::max<int64_t>(4096, (m + 7) / 8);
-  piece_points = std::min(piece_points, m);
-  const int npieces = (int)((m + piece_points - 1) / piece_points);
+  const int64_t piece = host_piece(m, piece_points);
+  const int npieces = (int)((m + piece - 1) / piece);
   const size_t row = (size_t)n * sizeof(double);
-  const size_t pbytes = (size_t)piece_points * row;
+  const size_t pdoubles = (size_t)piece * n;
   const size_t nparams = (func == CHESSFAD_FLETCHER_POWELL) ? (size_t)2 * n * n + n : 0;
 
-  cudaStream_t ss[2] = {nullptr, nullptr};
-  cudaEvent_t ready = nullptr, done[2] = {nullptr, nullptr};
-  double* d_buf = nullptr;
+  enum { H2D = 0, KRN = 1, D2H = 2 };
+  cudaStream_t ss[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ready = nullptr, ev[3][kHostSets] = {};
+  double* d_buf = (double*)workspace;
+  const bool own = d_buf == nullptr;
   cudaError_t e = cudaSuccess;
   auto ok = [&](cudaError_t x) { if (e == cudaSuccess) e = x; return e == cudaSuccess; };
-  // two buffer sets (points, vecs, out) so piece p+1 copies while piece p computes
-  const size_t total = 2 * 3 * pbytes + nparams * sizeof(double);
-  if (ok(cudaStreamCreateWithFlags(&ss[0], cudaStreamNonBlocking)) &&
-      ok(cudaStreamCreateWithFlags(&ss[1], cudaStreamNonBlocking)) &&
-      ok(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming)) &&
-      ok(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming)) &&
-      ok(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming)) &&
-      ok(cudaMallocAsync((void**)&d_buf, total, s0))) {
-    double* d_params = d_buf + 6 * (pbytes / sizeof(double));
+  for (int k = 0; k < 3; k++) ok(cudaStreamCreateWithFlags(&ss[k], cudaStreamNonBlocking));
+  ok(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  for (int k = 0; k < 3; k++)
+    for (int b = 0; b < kHostSets; b++) ok(cudaEventCreateWithFlags(&ev[k][b], cudaEventDisableTiming));
+  if (own) ok(cudaMallocAsync((void**)&d_buf, need, s0));
+  if (e == cudaSuccess) {
+    double* d_params = d_buf + (size_t)kHostSets * 3 * pdoubles;
     if (nparams) ok(cudaMemcpyAsync(d_params, params, nparams * sizeof(double), cudaMemcpyHostToDevice, s0));
     ok(cudaEventRecord(ready, s0));
-    ok(cudaStreamWaitEvent(ss[0], ready, 0));
-    ok(cudaStreamWaitEvent(ss[1], ready, 0));
+    for (int k = 0; k < 3; k++) ok(cudaStreamWaitEvent(ss[k], ready, 0));
     for (int p = 0; p < npieces && e == cudaSuccess; p++) {
-      const int b = p & 1;
-      cudaStream_t s = ss[b];
-      double* dp = d_buf + (size_t)(3 * b) * (pbytes / sizeof(double));
-      double* dv = dp + pbytes / sizeof(double);
-      double* dout = dv + pbytes / sizeof(double);
-      const int64_t e0 = (int64_t)p * piece_points;
-      const int64_t cnt = std::min(piece_points, m - e0);
+      const int b = p % kHostSets;
+      double* dp = d_buf + (size_t)(3 * b) * pdoubles;
+      double* dv = dp + pdoubles;
+      double* dout = dv + pdoubles;
+      const int64_t e0 = (int64_t)p * piece;
+      const int64_t cnt = std::min(piece, m - e0);
       const size_t bytes = (size_t)cnt * row;
-      // same-stream ordering protects buffer set b (its previous D2H precedes these copies)
-      ok(cudaMemcpyAsync(dp, points + e0 * n, bytes, cudaMemcpyHostToDevice, s));
-      ok(cudaMemcpyAsync(dv, vecs + e0 * n, bytes, cudaMemcpyHostToDevice, s));
+      if (p >= kHostSets) ok(cudaStreamWaitEvent(ss[H2D], ev[D2H][b], 0));  // set b drained
+      ok(cudaMemcpyAsync(dp, points + e0 * n, bytes, cudaMemcpyHostToDevice, ss[H2D]));
+      ok(cudaMemcpyAsync(dv, vecs + e0 * n, bytes, cudaMemcpyHostToDevice, ss[H2D]));
+      ok(cudaEventRecord(ev[H2D][b], ss[H2D]));
+      ok(cudaStreamWaitEvent(ss[KRN], ev[H2D][b], 0));
       if (e == cudaSuccess) {
-        const int r = run<MODE_HVP>(func, n, csize, cnt, dp, dv, dout, nparams ? d_params : nullptr, s);
+        const int r = run<MODE_HVP>(func, n, csize, cnt, dp, dv, dout, nparams ? d_params : nullptr, ss[KRN]);
         if (r != CHESSFAD_OK) e = cudaErrorLaunchFailure;
       }
-      ok(cudaMemcpyAsync(out + e0 * n, dout, bytes, cudaMemcpyDeviceToHost, s));
+      ok(cudaEventRecord(ev[KRN][b], ss[KRN]));
+      ok(cudaStreamWaitEvent(ss[D2H], ev[KRN][b], 0));
+      ok(cudaMemcpyAsync(out + e0 * n, dout, bytes, cudaMemcpyDeviceToHost, ss[D2H]));
+      ok(cudaEventRecord(ev[D2H][b], ss[D2H]));
     }
-    ok(cudaEventRecord(done[0], ss[0]));
-    ok(cudaEventRecord(done[1], ss[1]));
-    ok(cudaStreamWaitEvent(s0, done[0], 0));
-    ok(cudaStreamWaitEvent(s0, done[1], 0));
-    ok(cudaFreeAsync(d_buf, s0));
+    for (int k = 0; k < 3; k++) {
+      ok(cudaEventRecord(ready, ss[k]));
+      ok(cudaStreamWaitEvent(s0, ready, 0));
+    }
+    if (own) ok(cudaFreeAsync(d_buf, s0));
     ok(cudaStreamSynchronize(s0));
   }
-  for (int b = 0; b < 2; b++) {
-    if (ss[b]) cudaStreamDestroy(ss[b]);
-    if (done[b]) cudaEventDestroy(done[b]);
+  for (int k = 0; k < 3; k++) {
+    if (ss[k]) cudaStreamDestroy(ss[k]);
+    for (int b = 0; b < kHostSets; b++)
+      if (ev[k][b]) cudaEventDestroy(ev[k][b]);
   }
   if (ready) cudaEventDestroy(ready);
   return e == cudaSuccess ? CHESSFAD_OK : CHESSFAD_ERR_CUDA;

@@ -135,3 +135,16 @@ def test_symmetric_support():
         assert chf.is_supported("rosenbrock", 16, 4, algo)
         assert chf.is_supported("fletcher_powell", 16, 4, algo)
     assert not chf.is_supported("rosenbrock", 16, 3, "sym_hvp")
+
+
+def test_host_workspace_contract(lib):
+    """chessfad_hvp_batch_host rejects a too-small caller workspace before touching the GPU;
+    the size query is monotone in m."""
+    import paper_2410_22575_b200 as chf
+    need = lib.chessfad_hvp_host_workspace_bytes(0, 16, 1 << 20, 0)
+    assert need >= 3 * 3 * (1 << 16) * 16 * 8
+    assert lib.chessfad_hvp_host_workspace_bytes(2, 16, 1000, 100) > lib.chessfad_hvp_host_workspace_bytes(0, 16, 1000, 100)
+    vp = ctypes.c_void_p
+    st = lib.chessfad_hvp_batch_host(0, 16, 4, 1000, vp(1), vp(1), vp(1), None, 0, vp(1), 16, None)
+    assert st == 1  # ERR_ARG
+    assert chf.STATUS[st] == "CHESSFAD_ERR_ARG"
