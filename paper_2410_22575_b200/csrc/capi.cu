@@ -18,7 +18,9 @@ namespace {
 constexpr int kMaxNReg = 256;  // register-hDual path: (3 or 5)*n*33*8 B of shared memory per CTA
 constexpr int kMaxNF3 = 128;   // F3 path: per-thread R0/R1 scratch of 128 doubles
 
-bool reg_chunk_compiled(int C) { return C == 1 || C == 2 || C == 4 || C == 8 || C == 16 || C == 32; }
+// hDual<32> needs > 255 registers (ptxas spills 400+ B) and measured ~25% slower than two
+// 16-column groups (profiles/r01/campaign1/time_cfg3n*.jsonl), so C >= 32 runs as groups of 16.
+bool reg_chunk_compiled(int C) { return C == 1 || C == 2 || C == 4 || C == 8 || C == 16; }
 
 // Register path, C outside the compiled set: the chunk is executed as C/c' column groups of
 // the largest compiled c' <= 16 dividing C.  By slot independence column k of a
@@ -80,7 +82,6 @@ cudaError_t dispatch_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s)
     case 4: return launch_reg<F, 4, MODE>(a, s);       \
     case 8: return launch_reg<F, 8, MODE>(a, s);       \
     case 16: return launch_reg<F, 16, MODE>(a, s);     \
-    case 32: return launch_reg<F, 32, MODE>(a, s);     \
   }                                                    \
   break;
   switch (func) {

@@ -1,4 +1,4 @@
-// inst_ackley.cu -- kernel instantiations for FUNC_ACKLEY (hDual<C> in registers), C in {1..32},
+// inst_ackley.cu -- kernel instantiations for FUNC_ACKLEY (hDual<C> in registers), C in {1,2,4,8,16},
 // all four modes (Alg 7, Alg 5, Alg 8, Alg 6).
 #include "launch.cuh"
 

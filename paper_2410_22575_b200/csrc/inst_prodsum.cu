@@ -1,4 +1,4 @@
-// inst_prodsum.cu -- kernel instantiations for FUNC_PRODSUM (hDual<C> in registers), C in {1..32},
+// inst_prodsum.cu -- kernel instantiations for FUNC_PRODSUM (hDual<C> in registers), C in {1,2,4,8,16},
 // all four modes (Alg 7, Alg 5, Alg 8, Alg 6).
 #include "launch.cuh"
 
