@@ -295,7 +295,7 @@ def main():
     assert torch.equal(Oh, out.cpu()), "host-buffer path disagrees with the device path"
     e2e = {"value": m_all / e2e_t, "unit": UNIT, "h2d_bytes_per_step": 2 * m * n * 8 + (
         0 if ph_params is None else ph_params.numel() * 8), "d2h_bytes_per_step": m * n * 8,
-        "ms_per_step": e2e_t * 1e3, "api": "chessfad_hvp_batch_host (2-stream H2D/kernel/D2H pipeline)"}
+        "ms_per_step": e2e_t * 1e3, "api": "chessfad_hvp_batch_host (3-stage H2D/kernel/D2H stream pipeline, pinned host memory)"}
 
     # ---- chunk sweep over the four functions (cfg2)
     from paper_2410_22575_b200.build import source_hash

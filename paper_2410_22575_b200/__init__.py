@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libchessfad.so")
+LIB_PATH = os.environ.get("CHESSFAD_LIB") or os.path.join(HERE, "libchessfad.so")  # override: experiments
 
 ROSENBROCK, ACKLEY, FLETCHER_POWELL, PRODSUM = 0, 1, 2, 3
 FUNCS = {"rosenbrock": ROSENBROCK, "ackley": ACKLEY, "fletcher_powell": FLETCHER_POWELL, "prodsum": PRODSUM}
@@ -41,7 +41,7 @@ def load(build_if_missing: bool = True):
         if _lib is not None:
             return _lib
         from . import build as _build
-        if build_if_missing and not _build.up_to_date():
+        if build_if_missing and not os.environ.get("CHESSFAD_LIB") and not _build.up_to_date():
             _build.build()
         if not os.path.exists(LIB_PATH):
             raise ChessfadError(5, f"{LIB_PATH} not built; run paper_2410_22575_b200/build.py")

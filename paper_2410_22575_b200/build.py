@@ -57,10 +57,10 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in _deps())
 
 
-def _compile(src: str) -> str:
-    name = os.path.splitext(os.path.basename(src))[0]
+def _compile(src: str, defines=(), tag: str = "") -> str:
+    name = os.path.splitext(os.path.basename(src))[0] + tag
     obj = os.path.join(BUILD, name + ".o")
-    cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
+    cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     with open(os.path.join(BUILD, f"ptxas_{name}.log"), "w") as f:
         f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
@@ -69,21 +69,26 @@ def _compile(src: str) -> str:
     return obj
 
 
-def build(force: bool = False, jobs: int | None = None) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, jobs: int | None = None, defines=(), out: str | None = None) -> str:
+    """Build the library; `defines`/`out` build an experimental variant elsewhere (tuning)."""
+    if not force and not defines and out is None and up_to_date():
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     srcs = sources()
+    tag = "_" + "_".join(d.replace("=", "") for d in defines) if defines else ""
     with cf.ThreadPoolExecutor(max_workers=jobs or min(len(srcs), os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(_compile, srcs))
-    tmp = LIB + f".tmp{os.getpid()}"
+        objs = list(ex.map(lambda f: _compile(f, defines, tag), srcs))
+    target = out or LIB
+    tmp = target + f".tmp{os.getpid()}"
     cmd = [_nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outp = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")), None)
+    print(build(force="--force" in sys.argv, defines=defs, out=outp))

@@ -77,6 +77,11 @@ CHF_INL void f3_fma(const double2& c, int kk, const V& v, double (&Ep)[KB], doub
   }
 }
 
+#ifndef CHF_F3_JUNROLL
+#define CHF_F3_JUNROLL 1
+#endif
+constexpr int kF3JUnroll = CHF_F3_JUNROLL;  // j-loop unroll of the shared-memory (A,B) path
+
 struct SlotVals {
   double sp, cp, sq, cq;
 };
@@ -88,6 +93,7 @@ CHF_INL void f3_sum_j(const ABShared& ab, int n, int kb, const Vals& vals, doubl
 #pragma unroll
     for (int kk = 0; kk < KB; kk++) f3_fma<KB, true>(ab.get(kb + kk, 0), kk, v, Ep, Eq);
   }
+#pragma unroll kF3JUnroll
   for (int j = 1; j < n; j++) {
     const SlotVals v = vals(j);
 #pragma unroll

@@ -112,8 +112,11 @@ CHF_INL RowSink<MODE> make_sink(const BatchArgs& p, int i, int64_t e, const doub
 }
 
 // ---------------------------------------------------------------- F1, F2, F4: hDual<C> in registers
+#ifndef CHF_REG_MINB
+#define CHF_REG_MINB 1  // min CTAs/SM hint of the register path (tuning experiments)
+#endif
 template <class F, int C, int MODE, int W>
-__global__ void __launch_bounds__(W * 32) hvp_reg_kernel(BatchArgs p, F f) {
+__global__ void __launch_bounds__(W * 32, CHF_REG_MINB) hvp_reg_kernel(BatchArgs p, F f) {
   constexpr bool TRIG = uses_trig2pi<F>::value;
   constexpr bool HESS = mode_hess(MODE);
   extern __shared__ double smem[];
@@ -181,8 +184,11 @@ constexpr int kF3RingJ = 8;  // j-values per cp.async stage of the (A, B) ring (
 
 // min CTAs/SM: 3 (<= 168 registers) with (A, B) in shared memory; 2 (<= 255) for the ring
 // path, whose 16 broadcast loads per j need registers to be batched ahead of their DFMAs
+#ifndef CHF_F3_SMEM_MINB
+#define CHF_F3_SMEM_MINB 3
+#endif
 template <int KB, int MODE, bool AB_SMEM, bool SLIM>
-__global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? 3 : 2)
+__global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? CHF_F3_SMEM_MINB : 2)
     hvp_f3_kernel(BatchArgs p, const double2* __restrict__ abT_g) {
   constexpr bool HESS = mode_hess(MODE);
   constexpr bool VEC_TILE = !HESS && !SLIM;
