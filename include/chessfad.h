@@ -95,6 +95,19 @@ int chessfad_sym_hessian_batch(int func, int n, int csize, int64_t m, const doub
                                const double *params, void *stream);
 
 /*
+ * NEXT-4 (beyond the paper): Alg 7 with row-channel hoisting.  Slots 0 and 1
+ * of every intermediate (f and df/dx_i) do not depend on the chunk, so they are computed once
+ * per (point, row) instead of once per (point, row, chunk).  The outputs are bit-identical to
+ * chessfad_hvp_batch (same operations in the same order); the executed FLOPs are BELOW the
+ * model count chessfad_model_flops_per_point_algo(.., CHESSFAD_ALGO_HVP_ROWHOIST) reports (the
+ * paper's), so rates quoted against the model are "effective".  Fletcher-Powell only (its
+ * slot-column schedule separates the phases); other functions return ERR_UNSUPPORTED.
+ * Arguments as chessfad_hvp_batch.
+ */
+int chessfad_hvp_batch_rowhoist(int func, int n, int csize, int64_t m, const double *points, const double *vecs,
+                                double *out, const double *params, void *stream);
+
+/*
  * End-to-end variant of chessfad_hvp_batch on HOST buffers: points, vecs, out (m x n) and
  * params are HOST pointers (pinned memory gives copy/compute overlap; pageable memory
  * works but serialises).  The batch is split into pieces of `piece_points` points
@@ -126,7 +139,8 @@ enum chessfad_algo {
   CHESSFAD_ALGO_HVP = 0,          /* Alg 7, chessfad_hvp_batch */
   CHESSFAD_ALGO_HESSIAN = 1,      /* Alg 5, chessfad_hessian_batch */
   CHESSFAD_ALGO_SYM_HVP = 2,      /* Alg 8, chessfad_sym_hvp_batch */
-  CHESSFAD_ALGO_SYM_HESSIAN = 3   /* Alg 6, chessfad_sym_hessian_batch */
+  CHESSFAD_ALGO_SYM_HESSIAN = 3,  /* Alg 6, chessfad_sym_hessian_batch */
+  CHESSFAD_ALGO_HVP_ROWHOIST = 4  /* Alg 7 + NEXT-4 row-channel hoisting, chessfad_hvp_batch_rowhoist */
 };
 
 /* 1 if (func, n, csize) runs for the given algorithm, else 0. */

@@ -18,11 +18,12 @@ ROSENBROCK, ACKLEY, FLETCHER_POWELL, PRODSUM = 0, 1, 2, 3
 FUNCS = {"rosenbrock": ROSENBROCK, "ackley": ACKLEY, "fletcher_powell": FLETCHER_POWELL, "prodsum": PRODSUM}
 STATUS = {0: "CHESSFAD_OK", 1: "CHESSFAD_ERR_ARG", 2: "CHESSFAD_ERR_CHUNK", 3: "CHESSFAD_ERR_FUNC",
           4: "CHESSFAD_ERR_UNSUPPORTED", 5: "CHESSFAD_ERR_CUDA"}
-ALGOS = {"hvp": 0, "hessian": 1, "sym_hvp": 2, "sym_hessian": 3}
+ALGOS = {"hvp": 0, "hessian": 1, "sym_hvp": 2, "sym_hessian": 3, "hvp_rowhoist": 4}
 EXPORTS = sorted(["chessfad_hvp_batch", "chessfad_hessian_batch", "chessfad_sym_hvp_batch", "chessfad_sym_hessian_batch",
                   "chessfad_hvp_batch_host", "chessfad_is_supported", "chessfad_is_supported_algo",
                   "chessfad_status_string", "chessfad_model_flops_per_point", "chessfad_model_flops_per_point_algo",
-                  "chessfad_fp64_probe", "chessfad_version", "chessfad_hvp_host_workspace_bytes"])
+                  "chessfad_fp64_probe", "chessfad_version", "chessfad_hvp_host_workspace_bytes",
+                  "chessfad_hvp_batch_rowhoist"])
 
 _lock = threading.Lock()
 _lib = None
@@ -51,6 +52,7 @@ def load(build_if_missing: bool = True):
             "chessfad_hvp_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_hessian_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_sym_hvp_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
+            "chessfad_hvp_batch_rowhoist": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_sym_hessian_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_is_supported_algo": (i32, [i32, i32, i32, i32]),
             "chessfad_model_flops_per_point_algo": (dbl, [i32, i32, i32, i32]),
@@ -129,6 +131,12 @@ def hvp_batch(func, points, vecs, csize: int, params=None, out=None, stream=None
 def sym_hvp_batch(func, points, vecs, csize: int, params=None, out=None, stream=None):
     """Same product with the symmetric chunked algorithm (Alg 8 SC-HESS-VEC, batched)."""
     return _hvp("chessfad_sym_hvp_batch", func, points, vecs, csize, params, out, stream)
+
+
+def hvp_batch_rowhoist(func, points, vecs, csize: int, params=None, out=None, stream=None):
+    """NEXT-4: Alg 7 with slots 0/1 computed once per row (Fletcher-Powell); bit-identical
+    to hvp_batch, fewer executed FLOPs than the model count."""
+    return _hvp("chessfad_hvp_batch_rowhoist", func, points, vecs, csize, params, out, stream)
 
 
 def hessian_batch(func, points, csize: int, params=None, out=None, stream=None):

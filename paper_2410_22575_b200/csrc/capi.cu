@@ -59,6 +59,7 @@ constexpr size_t kSmemMax = 227 * 1024;
 
 int supported(int func, int n, int csize, int mode) {
   (void)csize;  // every C | n runs (F3: runtime C; register path: reg_kernel_chunk)
+  if (mode == MODE_HVP_ROWHOIST && func != CHESSFAD_FLETCHER_POWELL) return 0;  // NEXT-4: F3 only
   if (func == CHESSFAD_FLETCHER_POWELL)  // n > 32 streams (A, B) in 8-column cp.async stages
     return n <= kMaxNF3 && (n <= 32 || n % kF3RingJ == 0) &&
            f3_smem_bytes(n, groups_for(n, kWarpsF3, mode), mode) <= kSmemMax;
@@ -117,7 +118,12 @@ int run(int func, int n, int csize, int64_t m, const double* points, const doubl
   a.vecs = vecs;
   a.out = out;
   a.params = params;
-  const cudaError_t e = (func == CHESSFAD_FLETCHER_POWELL) ? dispatch_f3<MODE>(a, s) : dispatch_reg<MODE>(func, csize, a, s);
+  cudaError_t e;
+  if constexpr (MODE == MODE_HVP_ROWHOIST) {
+    e = (func == CHESSFAD_FLETCHER_POWELL) ? dispatch_f3<MODE>(a, s) : cudaErrorInvalidValue;
+  } else {
+    e = (func == CHESSFAD_FLETCHER_POWELL) ? dispatch_f3<MODE>(a, s) : dispatch_reg<MODE>(func, csize, a, s);
+  }
   return e == cudaSuccess ? CHESSFAD_OK : CHESSFAD_ERR_CUDA;
 }
 
@@ -165,6 +171,11 @@ int chessfad_sym_hvp_batch(int func, int n, int csize, int64_t m, const double* 
 int chessfad_sym_hessian_batch(int func, int n, int csize, int64_t m, const double* points, double* hess,
                                const double* params, void* stream) {
   return batch_entry<MODE_SYM_HESS>(func, n, csize, m, points, nullptr, hess, params, stream);
+}
+
+int chessfad_hvp_batch_rowhoist(int func, int n, int csize, int64_t m, const double* points, const double* vecs,
+                                double* out, const double* params, void* stream) {
+  return batch_entry<MODE_HVP_ROWHOIST>(func, n, csize, m, points, vecs, out, params, stream);
 }
 
 namespace {
@@ -267,11 +278,11 @@ int chessfad_is_supported(int func, int n, int csize) {
 }
 
 int chessfad_is_supported_algo(int func, int n, int csize, int algo) {
-  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_SYM_HESSIAN) return 0;
+  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_HVP_ROWHOIST) return 0;
   if (validate(func, n, csize, 0, false, func == CHESSFAD_FLETCHER_POWELL ? (const void*)1 : nullptr, nullptr,
                nullptr, nullptr))
     return 0;
-  static const int mode_of[4] = {MODE_HVP, MODE_HESS, MODE_SYM_HVP, MODE_SYM_HESS};
+  static const int mode_of[5] = {MODE_HVP, MODE_HESS, MODE_SYM_HVP, MODE_SYM_HESS, MODE_HVP_ROWHOIST};
   return supported(func, n, csize, mode_of[algo]);
 }
 
@@ -288,7 +299,7 @@ const char* chessfad_status_string(int status) {
 }
 
 double chessfad_model_flops_per_point_algo(int func, int n, int csize, int algo) {
-  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_SYM_HESSIAN) return -1.0;
+  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_HVP_ROWHOIST) return -1.0;
   if (validate(func, n, csize, 0, false, (const void*)1, nullptr, nullptr, nullptr)) return -1.0;
   const double C = csize, N = n;
   // per-evaluation hDual op counts of the canonical forms (DESIGN.md op table)
@@ -303,7 +314,7 @@ double chessfad_model_flops_per_point_algo(int func, int n, int csize, int algo)
   const bool sym = algo == CHESSFAD_ALGO_SYM_HVP || algo == CHESSFAD_ALGO_SYM_HESSIAN;
   const double evals = sym ? N * (N / C + 1) / 2 : N * N / C;
   // HVP dot: every H_ij v_j term once (Alg 8: n(n+C)/2 direct + n(n-C)/2 mirrored) = 2n^2
-  const bool hvp = algo == CHESSFAD_ALGO_HVP || algo == CHESSFAD_ALGO_SYM_HVP;
+  const bool hvp = algo == CHESSFAD_ALGO_HVP || algo == CHESSFAD_ALGO_SYM_HVP || algo == CHESSFAD_ALGO_HVP_ROWHOIST;
   return evals * per_eval + (hvp ? 2 * N * N : 0.0);
 }
 

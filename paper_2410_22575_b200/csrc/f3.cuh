@@ -126,16 +126,12 @@ CHF_INL void f3_sum_j(const ABRing<KB, JC>& ab, int n, int kb, const Vals& vals,
   }
 }
 
-// One evaluation f<hDual<C>>(CHUNK-INIT(i, cs)) for this lane's point (Alg 4 + Fig. 1).
-// For each column l in ascending order, sink(cs + l, d2f/dx_i dx_{cs+l}) consumes the
-// second-order slot C+2+l (the chunk dot of Alg 7, the store of Alg 5, the scatter of Alg 8).
-// sa/ca: sin/cos of the lane's coordinates, element j at [j * stride]; Es: E*.
-// R0/R1: per-thread scratch (n doubles).
-template <int KB, class AB, class Sink>
-CHF_INL void f3_eval(int n, int C, int i, int cs, const double* __restrict__ sa,
-                     const double* __restrict__ ca, int stride, const AB& ab,
-                     const double* __restrict__ Es, double* R0, double* R1, Sink&& sink) {
-  // ---------------- phase A: slots 0 and 1
+// Phase A of an evaluation: slots 0 and 1 of every residual r_k = E*_k - E_k into R0/R1.
+// It depends on the point and the row i only -- not on the chunk -- which is what the
+// NEXT-4 hoisted variant exploits (computed once per row instead of once per chunk).
+template <int KB, class AB>
+CHF_INL void f3_phase_a(int n, int i, const double* __restrict__ sa, const double* __restrict__ ca, int stride,
+                        const AB& ab, const double* __restrict__ Es, double* R0, double* R1) {
   // sin(y_j) = <sin a, cos a * y1, ...>;  cos(y_j) = <cos a, -sin a * y1, ...>
   auto valsA = [&](int j) {
     const double s0 = sa[j * stride], c0 = ca[j * stride];
@@ -153,8 +149,14 @@ CHF_INL void f3_eval(int n, int C, int i, int cs, const double* __restrict__ sa,
     }
   }
   // f slots 0/1 (f = sum_k r_k * r_k) are dead for the HVP and the Hessian.
+}
 
-  // ---------------- phase B: one column at a time
+// Phase B: the C columns of the chunk starting at cs, given R0/R1 of this row.  For each
+// column l in ascending order, sink(cs + l, d2f/dx_i dx_{cs+l}) consumes the second-order
+// slot C+2+l (the chunk dot of Alg 7, the store of Alg 5, the scatter of Alg 8).
+template <int KB, class AB, class Sink>
+CHF_INL void f3_phase_b(int n, int C, int i, int cs, const double* __restrict__ sa, const double* __restrict__ ca,
+                        int stride, const AB& ab, const double* R0, const double* R1, Sink&& sink) {
   for (int c = 0; c < C; c++) {
     const int col = cs + c;
     // sin: g' = cos a, g'' = -sin a;   cos: g' = -sin a, g'' = -cos a
@@ -178,6 +180,17 @@ CHF_INL void f3_eval(int n, int C, int i, int cs, const double* __restrict__ sa,
     }
     sink(col, fC);
   }
+}
+
+// One evaluation f<hDual<C>>(CHUNK-INIT(i, cs)) for this lane's point (Alg 4 + Fig. 1):
+// phase A then phase B.  sa/ca: sin/cos of the lane's coordinates (element j at
+// [j * stride]); Es: E*; R0/R1: per-thread scratch (n doubles).
+template <int KB, class AB, class Sink>
+CHF_INL void f3_eval(int n, int C, int i, int cs, const double* __restrict__ sa,
+                     const double* __restrict__ ca, int stride, const AB& ab,
+                     const double* __restrict__ Es, double* R0, double* R1, Sink&& sink) {
+  f3_phase_a<KB>(n, i, sa, ca, stride, ab, Es, R0, R1);
+  f3_phase_b<KB>(n, C, i, cs, sa, ca, stride, ab, R0, R1, sink);
 }
 
 }  // namespace chessfad

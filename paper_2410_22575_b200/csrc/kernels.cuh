@@ -30,7 +30,10 @@
 
 namespace chessfad {
 
-enum { MODE_HVP = 0, MODE_HESS = 1, MODE_SYM_HVP = 2, MODE_SYM_HESS = 3 };
+// MODE_HVP_ROWHOIST (NEXT-4, F3 only): Alg 7 with phase A (slots 0/1 of the residuals, which
+// do not depend on the chunk) computed once per row instead of once per chunk; outputs are
+// bit-identical to MODE_HVP, executed FLOPs are below the model count.
+enum { MODE_HVP = 0, MODE_HESS = 1, MODE_SYM_HVP = 2, MODE_SYM_HESS = 3, MODE_HVP_ROWHOIST = 4 };
 __host__ __device__ constexpr bool mode_hess(int M) { return M == MODE_HESS || M == MODE_SYM_HESS; }
 __host__ __device__ constexpr bool mode_sym(int M) { return M == MODE_SYM_HVP || M == MODE_SYM_HESS; }
 
@@ -84,7 +87,7 @@ struct RowSink {
   int n;
   bool mirror;      // symmetric modes: this chunk lies strictly after row i's chunk
   CHF_INL void operator()(int col, double h) {
-    if (MODE == MODE_HVP || MODE == MODE_SYM_HVP) {
+    if (MODE == MODE_HVP || MODE == MODE_SYM_HVP || MODE == MODE_HVP_ROWHOIST) {
       res = res + h * v[col * vs];
       if (MODE == MODE_SYM_HVP && mirror) s_res[col * kPad] = s_res[col * kPad] + h * vi;
     } else if (hrow) {
@@ -239,12 +242,24 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? CHF_F3_SMEM_MINB : 2)
   for (int i = warp / G; i < n; i += rstep) {
     const int scn = i / C;
     RowSink<MODE> sink = make_sink<MODE>(p, i, e, v, o, VEC_TILE ? kPad : 1);
+    if (MODE == MODE_HVP_ROWHOIST) {  // NEXT-4: phase A once per row
+      if (AB_SMEM)
+        f3_phase_a<KB>(n, i, sa, ca, kPad, ABShared{s_ab, n}, Es, R0, R1);
+      else
+        f3_phase_a<KB>(n, i, sa, ca, kPad, ring, Es, R0, R1);
+    }
     for (int j = mode_sym(MODE) ? scn : 0; j < nchunk; j++) {
       sink.mirror = j > scn;
-      if (AB_SMEM)
+      if (MODE == MODE_HVP_ROWHOIST) {
+        if (AB_SMEM)
+          f3_phase_b<KB>(n, C, i, j * C, sa, ca, kPad, ABShared{s_ab, n}, R0, R1, sink);
+        else
+          f3_phase_b<KB>(n, C, i, j * C, sa, ca, kPad, ring, R0, R1, sink);
+      } else if (AB_SMEM) {
         f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ABShared{s_ab, n}, Es, R0, R1, sink);
-      else
+      } else {
         f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ring, Es, R0, R1, sink);
+      }
     }
     if (!HESS) {
       if (SLIM) {

@@ -90,7 +90,8 @@ CHF_FOR_C(CHF_DECL_REG, FUNC_ACKLEY)
 CHF_FOR_C(CHF_DECL_REG, FUNC_PRODSUM)
 
 #define CHF_DECL_F31(KB, AB, M) extern template cudaError_t launch_f3<KB, M, AB>(BatchArgs, cudaStream_t);
-#define CHF_DECL_F3(KB) CHF_FOR_MODE(CHF_DECL_F31, KB, false) CHF_FOR_MODE(CHF_DECL_F31, KB, true)
+#define CHF_DECL_F3(KB) CHF_FOR_MODE(CHF_DECL_F31, KB, false) CHF_FOR_MODE(CHF_DECL_F31, KB, true) \
+  CHF_DECL_F31(KB, false, MODE_HVP_ROWHOIST) CHF_DECL_F31(KB, true, MODE_HVP_ROWHOIST)
 CHF_DECL_F3(1) CHF_DECL_F3(2) CHF_DECL_F3(4) CHF_DECL_F3(8) CHF_DECL_F3(16)
 
 }  // namespace chessfad

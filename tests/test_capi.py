@@ -148,3 +148,13 @@ def test_host_workspace_contract(lib):
     st = lib.chessfad_hvp_batch_host(0, 16, 4, 1000, vp(1), vp(1), vp(1), None, 0, vp(1), 16, None)
     assert st == 1  # ERR_ARG
     assert chf.STATUS[st] == "CHESSFAD_ERR_ARG"
+
+
+def test_rowhoist_contract():
+    """NEXT-4 entry point: F3 only; its model count is the paper's Alg 7 count."""
+    import paper_2410_22575_b200 as chf
+    assert chf.is_supported("fletcher_powell", 16, 4, "hvp_rowhoist")
+    assert chf.is_supported("fletcher_powell", 64, 16, "hvp_rowhoist")
+    assert not chf.is_supported("rosenbrock", 16, 4, "hvp_rowhoist")
+    assert chf.model_flops_per_point("fletcher_powell", 16, 4, algo="hvp_rowhoist") == \
+        chf.model_flops_per_point("fletcher_powell", 16, 4)

@@ -271,3 +271,22 @@ def test_sym_hessian_parity(chf, func):
         assert np.array_equal(Hs[:, upper], Hf[:, upper])
         lower = blk[:, None] > blk[None, :]
         assert np.array_equal(Hs[:, lower], Hs.transpose(0, 2, 1)[:, lower])
+
+
+# ------------------------------------------------------------ NEXT-4: row-channel hoisting (F3)
+@pytest.mark.parametrize("n,m", [(16, 700), (64, 40)])
+def test_rowhoist_bitwise_equal(chf, n, m):
+    """Phase A computed once per row gives the SAME bits as once per chunk (same ops, same
+    order), and matches the oracle."""
+    P, V = synth.points(17, n, m), synth.vectors(17, n, m)
+    params = synth.fp_params_flat(0, n)
+    dev = torch.device("cuda")
+    p, v, pr = (torch.from_numpy(x).to(dev) for x in (P, V, params))
+    ref, sabs = oracle.hvp_batch("fletcher_powell", P, V, n // 4 if n > 16 else 4, params)
+    for C in (1, 4, n):
+        a = chf.hvp_batch("fletcher_powell", p, v, C, pr).cpu().numpy()
+        b = chf.hvp_batch_rowhoist("fletcher_powell", p, v, C, pr).cpu().numpy()
+        assert np.array_equal(a, b)
+        _check(b, ref, sabs)
+    with pytest.raises(chf.ChessfadError, match="UNSUPPORTED"):
+        chf.hvp_batch_rowhoist("rosenbrock", p, v, 4)
