@@ -12,12 +12,13 @@ import paper_2410_22575_b200 as chf  # noqa: E402
 import synth  # noqa: E402
 
 dev = torch.device("cuda", 0)
-for n, m in ((16, 77), (64, 40)):
+small = os.environ.get("SANITIZE_SMALL") == "1"  # racecheck: fewer, smaller launches
+for n, m in (((16, 33), (64, 5)) if small else ((16, 77), (64, 40))):
     p = torch.from_numpy(synth.points(0, n, m)).to(dev)
     v = torch.from_numpy(synth.vectors(0, n, m)).to(dev)
     pr = torch.from_numpy(synth.fp_params_flat(0, n)).to(dev)
     for f in ("rosenbrock", "ackley", "fletcher_powell", "prodsum"):
-        for C in (4, 16):
+        for C in ((16,) if small else (4, 16)):
             par = pr if f == "fletcher_powell" else None
             for algo, fn in (("hvp", chf.hvp_batch), ("sym_hvp", chf.sym_hvp_batch)):
                 if chf.is_supported(f, n, C, algo):
