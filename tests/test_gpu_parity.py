@@ -290,3 +290,54 @@ def test_rowhoist_bitwise_equal(chf, n, m):
         _check(b, ref, sabs)
     with pytest.raises(chf.ChessfadError, match="UNSUPPORTED"):
         chf.hvp_batch_rowhoist("rosenbrock", p, v, 4)
+
+
+# ------------------------------------------------------------ BASELINE full sizes, sampled
+def _sampled_check(chf, func, n, m, C, algo="hvp", nsample=24, seed=0):
+    P, V = synth.points(seed, n, m), synth.vectors(seed, n, m)
+    params = _params(func, n)
+    dev = torch.device("cuda")
+    p, v = torch.from_numpy(P).to(dev), torch.from_numpy(V).to(dev)
+    pr = None if params is None else torch.from_numpy(params).to(dev)
+    idx = np.unique(np.concatenate([[0, m - 1], np.linspace(0, m - 1, nsample).astype(np.int64)]))
+    if algo in ("hessian", "sym_hessian"):
+        fn = chf.hessian_batch if algo == "hessian" else chf.sym_hessian_batch
+        H = fn(func, p, C, pr)
+        got = H[torch.from_numpy(idx).to(dev)].cpu().numpy()
+        del H
+        ref = oracle.hessian_batch(func, P[idx], C, params)
+        scale = np.abs(ref).reshape(idx.size, -1).max(axis=1)
+        assert (np.abs(got - ref).reshape(idx.size, -1).max(axis=1) / scale).max() <= TIGHT
+    else:
+        fn = {"hvp": chf.hvp_batch, "sym_hvp": chf.sym_hvp_batch}[algo]
+        got = fn(func, p, v, C, pr)[torch.from_numpy(idx).to(dev)].cpu().numpy()
+        ref, sabs = oracle.hvp_batch(func, P[idx], V[idx], C, params)
+        _check(got, ref, sabs)
+
+
+@pytest.mark.parametrize("func", ["rosenbrock", "ackley", "prodsum"])
+@pytest.mark.parametrize("n", [64, 128])
+def test_config3_full_size_sampled(chf, func, n):
+    """cfg3: n = 64 / 128, m = 2^20 (Fletcher-Powell below), C = 16 and C = n."""
+    for C in (16, n):
+        _sampled_check(chf, func, n, 1 << 20, C, nsample=16)
+
+
+@pytest.mark.parametrize("n,m", [(64, 1 << 16), (128, 1 << 13)])
+def test_config3_fletcher_powell_sampled(chf, n, m):
+    """cfg3 Fletcher-Powell at the reduced m the bench sweeps use (2.3-4.4 GFLOP per point at
+    n = 128 makes m = 2^20 a minutes-long launch)."""
+    _sampled_check(chf, "fletcher_powell", n, m, 16, nsample=8)
+
+
+@pytest.mark.parametrize("func", FUNCS)
+def test_config4_hessian_full_size_sampled(chf, func):
+    """cfg4: full Hessians at n = 32, m = 2^18 (2 GiB of output), Alg 5 and Alg 6."""
+    for algo in ("hessian", "sym_hessian"):
+        _sampled_check(chf, func, 32, 1 << 18, 8, algo=algo, nsample=12)
+
+
+def test_config5_full_size_sampled(chf):
+    """cfg5: n = 16, m = 2^23 on one GPU (the strong-scaling total), C = 16."""
+    _sampled_check(chf, "rosenbrock", 16, 1 << 23, 16, nsample=32)
+    _sampled_check(chf, "rosenbrock", 16, 1 << 23, 4, algo="sym_hvp", nsample=32)
