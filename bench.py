@@ -370,7 +370,9 @@ def main():
                                        "(sm_max_mhz, MEASURED_PEAKS.json); DESIGN.md",
                          "model_flops_per_point": flops_pt,
                          "fp64_probe_tflops": probe_tf, "frac_of_probe": achieved / probe_tf},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps, "clocks": clocks, "parity": parity,
+            "cpu_baseline": cpu, "e2e": e2e,
+            # one kernel per call; F3 with n > 32 adds the (A, B) interleave kernel
+            "gpu_launches": args.steps * (2 if (args.func == "fletcher_powell" and n > 32) else 1), "clocks": clocks, "parity": parity,
             "gather": gather, "sweep": sweep,
         }
         print(json.dumps(line), flush=True)
