@@ -297,24 +297,37 @@ def main():
         0 if ph_params is None else ph_params.numel() * 8), "d2h_bytes_per_step": m * n * 8,
         "ms_per_step": e2e_t * 1e3, "api": "chessfad_hvp_batch_host (3-stage H2D/kernel/D2H stream pipeline, pinned host memory)"}
 
-    # ---- chunk sweep over the four functions (cfg2)
+    # ---- chunk sweep over the four functions (cfg2), Alg 7 and the NEXT rows
     from paper_2410_22575_b200.build import source_hash
     src_hash = source_hash()
     sweep = []
+    algo_fn = {"hvp": chf.hvp_batch, "sym_hvp": chf.sym_hvp_batch, "hvp_rowhoist": chf.hvp_batch_rowhoist}
     if not args.no_sweep:
-        for f in FUNCS:
-            for c in (1, 2, 4, 8, 16):
-                if n % c or not chf.is_supported(f, n, c):
-                    continue
-                ks = 10
-                tt = timed(f, c, ks, 3) / ks
-                fl = chf.model_flops_per_point(f, n, c)
-                exs = executed_entry(f, n, c, src_hash)
-                sweep.append({"func": f, "csize": c, "hvp_per_s": m_all / tt, "ms": tt * 1e3,
-                              "model_tflops_effective": m * fl / tt / 1e12,
-                              "executed_tflops": None if exs is None else m * exs["executed_flops_per_point"] / tt / 1e12,
-                              "executed_frac": None if exs is None else
-                              m * exs["executed_flops_per_point"] / tt / 1e12 / peak_tf})
+        for algo, fnb in algo_fn.items():
+            for f in FUNCS:
+                for c in (1, 2, 4, 8, 16):
+                    if n % c or not chf.is_supported(f, n, c, algo):
+                        continue
+                    for _ in range(3):
+                        fnb(f, pts, vec, c, params[f], out=out)
+                    torch.cuda.synchronize()
+                    barrier()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    ks = 10
+                    e0.record(stream)
+                    for _ in range(ks):
+                        fnb(f, pts, vec, c, params[f], out=out)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    tt = max_over_ranks(e0.elapsed_time(e1) / 1e3) / ks
+                    fl = chf.model_flops_per_point(f, n, c, algo=algo)
+                    exs = executed_entry(f, n, c, src_hash, algo)
+                    sweep.append({"algo": algo, "func": f, "csize": c, "hvp_per_s": m_all / tt, "ms": tt * 1e3,
+                                  "model_tflops_effective": m * fl / tt / 1e12,
+                                  "executed_tflops": None if exs is None else
+                                  m * exs["executed_flops_per_point"] / tt / 1e12,
+                                  "executed_frac": None if exs is None else
+                                  m * exs["executed_flops_per_point"] / tt / 1e12 / peak_tf})
 
     # ---- CPU baseline: the oracle on the host cores, rank 0 at N=1 only
     cpu = None

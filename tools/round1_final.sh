@@ -1,0 +1,31 @@
+#!/bin/bash
+# Final round-1 measurement campaign (one B200) for the committed build.
+set -x
+O=gpurun_out
+mkdir -p $O
+rm -f $O/executed_flops.json
+timeout 1500 python -m pytest tests -m gpu -q > $O/final_pytest.log 2>&1; tail -3 $O/final_pytest.log
+# executed-FLOP tables (ncu): counts per point do not depend on m
+bash tools/ncu_executed.sh cfg2 --n 16 --m 262144
+bash tools/ncu_executed.sh cfg2sym --n 16 --m 262144 --algo sym_hvp
+bash tools/ncu_executed.sh cfg2hoist --n 16 --m 262144 --algo hvp_rowhoist --funcs fletcher_powell
+bash tools/ncu_executed.sh cfg4 --n 32 --m 65536 --algo hessian --csizes 1 2 4 8 16 32
+bash tools/ncu_executed.sh cfg4sym --n 32 --m 65536 --algo sym_hessian --csizes 1 2 4 8 16 32
+bash tools/ncu_executed.sh cfg3n64 --n 64 --m 131072 --funcs rosenbrock ackley prodsum --csizes 1 2 4 8 16 32 64
+bash tools/ncu_executed.sh cfg3n64f3 --n 64 --m 16384 --funcs fletcher_powell --csizes 1 4 16 64
+bash tools/ncu_executed.sh cfg3n128 --n 128 --m 65536 --funcs rosenbrock ackley prodsum --csizes 1 2 4 8 16 32 64 128
+bash tools/ncu_executed.sh cfg3n128f3 --n 128 --m 4096 --funcs fletcher_powell --csizes 1 8 32 128
+# event-timed sweeps
+timeout 600 python tools/sweep_bench.py --n 16 --m 1048576 --algo hvp > $O/time_cfg2.jsonl
+timeout 600 python tools/sweep_bench.py --n 16 --m 1048576 --algo sym_hvp > $O/time_cfg2sym.jsonl
+timeout 600 python tools/sweep_bench.py --n 16 --m 1048576 --algo hvp_rowhoist --funcs fletcher_powell > $O/time_cfg2hoist.jsonl
+timeout 900 python tools/sweep_bench.py --n 32 --m 262144 --algo hessian > $O/time_cfg4.jsonl
+timeout 900 python tools/sweep_bench.py --n 32 --m 262144 --algo sym_hessian > $O/time_cfg4sym.jsonl
+timeout 1200 python tools/sweep_bench.py --n 64 --m 1048576 --algo hvp --f3-m 65536 > $O/time_cfg3n64.jsonl
+timeout 1500 python tools/sweep_bench.py --n 128 --m 1048576 --algo hvp --f3-m 8192 --min-seconds 0.1 > $O/time_cfg3n128.jsonl
+# launch list of the bench command and a full capture of the headline kernel
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_bench.csv python bench.py --steps 5 --warmup 3 --no-sweep --no-cpu --e2e-steps 1 > $O/launches_bench_out.json 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:hvp_reg -c 1 -o $O/prof_headline python tools/profile_sweep.py --funcs rosenbrock --csizes 16 > /dev/null 2>&1
+timeout 600 python bench.py > $O/bench_final.json 2> $O/bench_final.err
+timeout 300 python tools/e2e_probe.py > $O/e2e_probe_final.jsonl 2>&1
+ls $O
