@@ -394,12 +394,12 @@ def main():
     return 0
 
 
-def executed_entry(func, n, C, src_hash, algo="hvp"):
+def executed_entry(func, n, C, src_hash, algo="hvp", path=None):
     """ncu-measured executed FLOPs/point of this build (profiles/executed_flops.json).  If the
     table was measured on an earlier build, its executed/model ratio is applied to this build's
     model count and the entry is marked stale (its 'basis' field says so)."""
     try:
-        tab = json.load(open(os.path.join(ROOT, "profiles", "executed_flops.json")))
+        tab = json.load(open(path or os.path.join(ROOT, "profiles", "executed_flops.json")))
     except Exception:
         return None
     key = f"{func} n={n} C={C}" + ("" if algo == "hvp" else f" {algo}")

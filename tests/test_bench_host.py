@@ -1,0 +1,43 @@
+"""Host-side logic of bench.py (no GPU): executed-FLOP accounting table lookup, stale-build
+fallback, NVML throttle-reason decoding and the workload description."""
+import argparse
+import json
+
+import bench
+
+
+def test_executed_entry_current_and_stale(tmp_path):
+    import paper_2410_22575_b200 as chf
+    model = chf.model_flops_per_point("rosenbrock", 16, 16)
+    tab = {"src_hash": "abc", "entries": {
+        "rosenbrock n=16 C=16": {"executed_flops_per_point": 0.5 * model, "model_flops_per_point": model,
+                                 "fp64_pipe_active_pct": 80.0, "dram_bytes_per_launch": 1.0, "m": 1},
+        "fletcher_powell n=16 C=4 sym_hvp": {"executed_flops_per_point": 10.0, "model_flops_per_point": 20.0,
+                                             "fp64_pipe_active_pct": 60.0, "dram_bytes_per_launch": 1.0, "m": 1}}}
+    p = tmp_path / "t.json"
+    p.write_text(json.dumps(tab))
+    e = bench.executed_entry("rosenbrock", 16, 16, "abc", path=str(p))
+    assert e["executed_flops_per_point"] == 0.5 * model and "this build" in e["basis"]
+    s = bench.executed_entry("rosenbrock", 16, 16, "other", path=str(p))
+    assert s["basis"].startswith("STALE") and abs(s["executed_flops_per_point"] - 0.5 * model) < 1e-6
+    assert bench.executed_entry("fletcher_powell", 16, 4, "abc", algo="sym_hvp", path=str(p)) is not None
+    assert bench.executed_entry("ackley", 16, 16, "abc", path=str(p)) is None
+    assert bench.executed_entry("ackley", 16, 16, "abc", path=str(tmp_path / "missing.json")) is None
+
+
+def test_peak_and_config():
+    tf, mhz = bench.fp64_nominal_tflops({"sm_max_mhz": 1965.0})
+    assert abs(tf - 148 * 64 * 2 * 1.965e9 / 1e12) < 1e-9 and mhz == 1965.0
+    a = argparse.Namespace(func="rosenbrock", n=16, csize=16, m=1 << 20, m_total=0)
+    c = bench.workload_config(a, 2)
+    assert c["global_points"] == 2 << 20 and "cfg2" in c["workload"]
+    a.m_total = 1 << 23
+    assert "cfg5" in bench.workload_config(a, 8)["workload"]
+
+
+def test_clock_reason_decoding():
+    cs = bench.ClockSampler.__new__(bench.ClockSampler)
+    cs.ok, cs.samples, cs.max_mhz = True, [1965, 1950, 1965], 1965
+    cs.reasons = 0x1 | 0x4 | 0x40
+    s = cs.summary()
+    assert s["sm_mhz"] == 1965 and s["reasons"] == ["sw_power_cap", "hw_thermal_slowdown"]
