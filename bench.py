@@ -329,6 +329,32 @@ def main():
                                   "executed_frac": None if exs is None else
                                   m * exs["executed_flops_per_point"] / tt / 1e12 / peak_tf})
 
+    # ---- the paper's own Fig. 2 L2 kernel design recompiled for sm_100a (comparison baseline)
+    paper_l2 = None
+    if chf.is_supported(args.func, n, C) and args.func in ("rosenbrock", "prodsum") and n in (2, 4, 8, 16):
+        best = None
+        for c in (1, 2, 4, 8, 16):
+            if n % c:
+                continue
+            try:
+                chf.hvp_batch_paper_l2(args.func, pts, vec, c, out=out)
+            except chf.ChessfadError:
+                continue
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(5):
+                chf.hvp_batch_paper_l2(args.func, pts, vec, c, out=out)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            tt = max_over_ranks(e0.elapsed_time(e1) / 1e3) / 5
+            if best is None or tt < best[1]:
+                best = (c, tt)
+        if best:
+            paper_l2 = {"kernel": "paper Fig. 2 L2 design (thread per instance x row x chunk, per-thread hDual y[n], "
+                                  "shared-memory reduction), recompiled for sm_100a", "best_csize": best[0],
+                        "hvp_per_s": m_all / best[1], "ms": best[1] * 1e3, "ours_over_paper_l2": best[1] / per_step}
+
     # ---- CPU baseline: the oracle on the host cores, rank 0 at N=1 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -386,7 +412,7 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e,
             # one kernel per call; F3 with n > 32 adds the (A, B) interleave kernel
             "gpu_launches": args.steps * (2 if (args.func == "fletcher_powell" and n > 32) else 1), "clocks": clocks, "parity": parity,
-            "gather": gather, "sweep": sweep,
+            "gather": gather, "paper_l2_baseline": paper_l2, "sweep": sweep,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

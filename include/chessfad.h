@@ -123,6 +123,17 @@ int chessfad_hvp_batch_host(int func, int n, int csize, int64_t m, const double 
                             double *out, const double *params, int64_t piece_points, void *workspace,
                             size_t workspace_bytes, void *stream);
 
+/*
+ * COMPARISON BASELINE, not the product path: the paper's own GPU design, Fig. 2 "L2"
+ * recompiled for sm_100a -- one thread per (instance, row, chunk), a
+ * materialised per-thread hDual<C> y[n] seed array, partial dots reduced through shared
+ * memory with __syncthreads.  Same result as chessfad_hvp_batch (within rounding).
+ * Rosenbrock and prodsum, n in {2, 4, 8, 16}, csize in {1, 2, 4, 8, 16}, csize | n; else
+ * ERR_UNSUPPORTED.  Device pointers, asynchronous on `stream`.
+ */
+int chessfad_hvp_batch_paper_l2(int func, int n, int csize, int64_t m, const double *points, const double *vecs,
+                                double *out, void *stream);
+
 /* Device workspace bytes chessfad_hvp_batch_host needs for (func, n, m, piece_points). */
 size_t chessfad_hvp_host_workspace_bytes(int func, int n, int64_t m, int64_t piece_points);
 

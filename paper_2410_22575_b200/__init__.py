@@ -23,7 +23,7 @@ EXPORTS = sorted(["chessfad_hvp_batch", "chessfad_hessian_batch", "chessfad_sym_
                   "chessfad_hvp_batch_host", "chessfad_is_supported", "chessfad_is_supported_algo",
                   "chessfad_status_string", "chessfad_model_flops_per_point", "chessfad_model_flops_per_point_algo",
                   "chessfad_fp64_probe", "chessfad_version", "chessfad_hvp_host_workspace_bytes",
-                  "chessfad_hvp_batch_rowhoist"])
+                  "chessfad_hvp_batch_rowhoist", "chessfad_hvp_batch_paper_l2"])
 
 _lock = threading.Lock()
 _lib = None
@@ -53,6 +53,7 @@ def load(build_if_missing: bool = True):
             "chessfad_hessian_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_sym_hvp_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_hvp_batch_rowhoist": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
+            "chessfad_hvp_batch_paper_l2": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_sym_hessian_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_is_supported_algo": (i32, [i32, i32, i32, i32]),
             "chessfad_model_flops_per_point_algo": (dbl, [i32, i32, i32, i32]),
@@ -137,6 +138,18 @@ def hvp_batch_rowhoist(func, points, vecs, csize: int, params=None, out=None, st
     """NEXT-4: Alg 7 with slots 0/1 computed once per row (Fletcher-Powell); bit-identical
     to hvp_batch, fewer executed FLOPs than the model count."""
     return _hvp("chessfad_hvp_batch_rowhoist", func, points, vecs, csize, params, out, stream)
+
+
+def hvp_batch_paper_l2(func, points, vecs, csize: int, out=None, stream=None):
+    """COMPARISON BASELINE: the paper's Fig. 2 L2 kernel design recompiled for sm_100a."""
+    import torch
+    m, n = points.shape
+    if out is None:
+        out = torch.empty_like(points)
+    st = load().chessfad_hvp_batch_paper_l2(_func(func), n, csize, m, _dev(points, "points"),
+                                            _dev(vecs, "vecs", (m, n)), _dev(out, "out", (m, n)), _stream_ptr(stream))
+    _check(st)
+    return out
 
 
 def hessian_batch(func, points, csize: int, params=None, out=None, stream=None):

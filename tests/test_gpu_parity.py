@@ -341,3 +341,17 @@ def test_config5_full_size_sampled(chf):
     """cfg5: n = 16, m = 2^23 on one GPU (the strong-scaling total), C = 16."""
     _sampled_check(chf, "rosenbrock", 16, 1 << 23, 16, nsample=32)
     _sampled_check(chf, "rosenbrock", 16, 1 << 23, 4, algo="sym_hvp", nsample=32)
+
+
+# ------------------------------------------------------------ the paper's Fig. 2 L2 design (comparison baseline)
+@pytest.mark.parametrize("func", ["rosenbrock", "prodsum"])
+@pytest.mark.parametrize("n", [2, 4, 8, 16])
+def test_paper_l2_baseline_parity(chf, func, n):
+    m = 777
+    P, V = synth.points(18, n, m), synth.vectors(18, n, m)
+    ref, sabs = oracle.hvp_batch(func, P, V, 1)
+    dev = torch.device("cuda")
+    p, v = torch.from_numpy(P).to(dev), torch.from_numpy(V).to(dev)
+    for C in divisors(n):
+        got = chf.hvp_batch_paper_l2(func, p, v, C).cpu().numpy()
+        _check(got, ref, sabs)
