@@ -433,10 +433,14 @@ def executed_entry(func, n, C, src_hash, algo="hvp", path=None):
     if ent is None:
         return None
     ent = dict(ent)
-    if tab.get("src_hash") == src_hash:
+    import paper_2410_22575_b200 as chf
+    from paper_2410_22575_b200.sass import sass_hash_for
+    cur = sass_hash_for(chf.LIB_PATH, ent["kernel"]) if ent.get("kernel") and ent.get("sass_hash") else None
+    if cur is not None and cur == ent["sass_hash"]:
+        ent["basis"] = f"ncu on identical kernel SASS ({cur})"
+    elif tab.get("src_hash") == src_hash:
         ent["basis"] = f"ncu on this build ({src_hash})"
     else:
-        import paper_2410_22575_b200 as chf
         ratio = ent["executed_flops_per_point"] / ent["model_flops_per_point"]
         ent["executed_flops_per_point"] = ratio * chf.model_flops_per_point(func, n, C, algo=algo)
         ent["basis"] = f"STALE: executed/model ratio {ratio:.3f} measured by ncu on build {tab.get('src_hash')}"

@@ -1,0 +1,74 @@
+"""Per-kernel SASS fingerprints of libchessfad.so (cuobjdump -sass + c++filt).
+
+The ncu-measured executed-FLOP table (profiles/executed_flops.json) is valid for exactly
+the SASS that was profiled; keying each entry by the sha256 of its kernel's SASS lets
+bench.py tell whether the shipped library still runs those instructions, independently of
+unrelated source edits.
+"""
+from __future__ import annotations
+
+import functools
+import hashlib
+import re
+import shutil
+import subprocess
+
+
+def _tool(name: str) -> str | None:
+    return shutil.which(name) or (f"/usr/local/cuda/bin/{name}" if name == "cuobjdump" else None)
+
+
+@functools.lru_cache(maxsize=4)
+def kernel_sass_hashes(lib_path: str) -> dict:
+    """{demangled kernel name: sha256(SASS)[:16]} for every kernel in lib_path ({} if the
+    tools are unavailable)."""
+    cuobjdump, cxxfilt = _tool("cuobjdump"), _tool("c++filt")
+    if not cuobjdump or not cxxfilt:
+        return {}
+    try:
+        sass = subprocess.run([cuobjdump, "-sass", lib_path], capture_output=True, text=True, timeout=120).stdout
+    except Exception:
+        return {}
+    funcs, name, body = {}, None, []
+    for line in sass.splitlines():
+        m = re.match(r"\s*Function : (\S+)", line)
+        if m:
+            if name:
+                funcs[name] = body
+            name, body = m.group(1), []
+        elif name and re.match(r"\s+/\*[0-9a-f]{4,}\*/", line):
+            body.append(re.sub(r"/\*[0-9a-f]+\*/", "", line).strip())
+    if name:
+        funcs[name] = body
+    mangled = list(funcs)
+    if not mangled:
+        return {}
+    dem = subprocess.run([cxxfilt], input="\n".join(mangled), capture_output=True, text=True).stdout.splitlines()
+    return {d.strip(): hashlib.sha256("\n".join(funcs[mn]).encode()).hexdigest()[:16] for mn, d in zip(mangled, dem)}
+
+
+def normalize(name: str) -> str:
+    """Comparable key for a kernel name as ncu prints it (base names, (int) casts, 1/0) and as
+    c++filt prints it (namespaces, true/false): name<template args>, no parameter list."""
+    name = re.sub(r"^void\s+", "", name.strip())
+    name = re.sub(r"\((int|bool|unsigned int)\)", "", name)
+    name = re.sub(r"\b\w+::", "", name)
+    name = re.sub(r"\btrue\b", "1", re.sub(r"\bfalse\b", "0", name))
+    name = re.sub(r"\s+", "", name)
+    depth = 0
+    for i, ch in enumerate(name):  # cut the parameter list after the template arguments
+        if ch == "<":
+            depth += 1
+        elif ch == ">":
+            depth -= 1
+        elif ch == "(" and depth == 0:
+            return name[:i]
+    return name
+
+
+def sass_hash_for(lib_path: str, kernel_name: str) -> str | None:
+    want = normalize(kernel_name)
+    for k, h in kernel_sass_hashes(lib_path).items():
+        if normalize(k) == want:
+            return h
+    return None

@@ -17,6 +17,7 @@ def load(csv_path, order_path):
             continue  # only the batch kernels (not the F3 (A,B) prep kernel)
         lid = int(r[ix["ID"]])
         per.setdefault(lid, {})[r[ix["Metric Name"]]] = float(r[ix["Metric Value"]].replace(",", ""))
+        per[lid]["__kernel"] = r[ix["Kernel Name"]]
     out = []
     for lid, (k, v) in enumerate(sorted(per.items())):
         if lid >= len(order):
@@ -27,7 +28,7 @@ def load(csv_path, order_path):
         model = float(fl.split("=")[1]) * m
         ex = 2 * v["sm__sass_thread_inst_executed_op_dfma_pred_on.sum"] + v["sm__sass_thread_inst_executed_op_dmul_pred_on.sum"] + v["sm__sass_thread_inst_executed_op_dadd_pred_on.sum"]
         t = v["gpu__time_duration.sum"] * 1e-9
-        out.append({"func": func, "n": n, "C": C, "m": m, "algo": algo, "time_ms": t * 1e3,
+        out.append({"func": func, "n": n, "C": C, "m": m, "algo": algo, "kernel": v["__kernel"], "time_ms": t * 1e3,
                     "model_flops": model, "executed_flops": ex, "executed_over_model": ex / model,
                     "fp64_warp_inst": v["sm__inst_executed_pipe_fp64.sum"],
                     "fp64_pipe_active_pct": v["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"],
@@ -46,22 +47,28 @@ def update_table(res, table_path):
     source hash of the build that was profiled)."""
     import os
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2410_22575_b200 import LIB_PATH
     from paper_2410_22575_b200.build import source_hash
+    from paper_2410_22575_b200.sass import sass_hash_for
     h = source_hash()
     try:
         tab = json.load(open(table_path))
     except Exception:
         tab = {}
-    if tab.get("src_hash") != h:
-        tab = {"src_hash": h, "entries": {}}
+    if tab.get("src_hash") != h:  # keep entries whose kernel SASS is unchanged
+        keep = {k: e for k, e in tab.get("entries", {}).items()
+                if e.get("sass_hash") and sass_hash_for(LIB_PATH, e.get("kernel", "")) == e["sass_hash"]}
+        tab = {"src_hash": h, "entries": keep}
     for r in res:
         key = f"{r['func']} n={r['n']} C={r['C']}" + ("" if r.get("algo", "hvp") == "hvp" else f" {r['algo']}")
         tab["entries"][key] = {"executed_flops_per_point": r["executed_flops"] / r["m"],
                                "model_flops_per_point": r["model_flops"] / r["m"],
                                "fp64_pipe_active_pct": r["fp64_pipe_active_pct"],
                                "dram_bytes_per_launch": r["dram_bytes"], "m": r["m"], "regs": r["regs"],
-                               "ncu_time_ms": r["time_ms"]}
-    tab["note"] = ("executed FP64 FLOPs = 2*DFMA + DMUL + DADD thread instructions (ncu "
+                               "ncu_time_ms": r["time_ms"], "kernel": r["kernel"],
+                               "sass_hash": sass_hash_for(LIB_PATH, r["kernel"])}
+    tab["note"] = ("entries are valid for the kernel SASS whose sha256 is sass_hash (paper_2410_22575_b200/sass.py); "
+                   "executed FP64 FLOPs = 2*DFMA + DMUL + DADD thread instructions (ncu "
                    "sm__sass_thread_inst_executed_op_{dfma,dmul,dadd}_pred_on.sum) per point, one launch each; "
                    "tools/profile_sweep.py under ncu, summarised by tools/summarize_sweep.py")
     json.dump(tab, open(table_path, "w"), indent=1, sort_keys=True)
