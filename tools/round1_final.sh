@@ -6,7 +6,7 @@ mkdir -p $O
 rm -f $O/executed_flops.json
 timeout 1500 python -m pytest tests -m gpu -q > $O/final_pytest.log 2>&1; tail -3 $O/final_pytest.log
 # executed-FLOP tables (ncu): counts per point do not depend on m
-bash tools/ncu_executed.sh cfg2 --n 16 --m 262144
+bash tools/ncu_executed.sh cfg2 --n 16 --m 1048576
 bash tools/ncu_executed.sh cfg2sym --n 16 --m 262144 --algo sym_hvp
 bash tools/ncu_executed.sh cfg2hoist --n 16 --m 262144 --algo hvp_rowhoist --funcs fletcher_powell
 bash tools/ncu_executed.sh cfg4 --n 32 --m 65536 --algo hessian --csizes 1 2 4 8 16 32
