@@ -76,6 +76,15 @@ int chessfad_hessian_batch(int func, int n, int csize, int64_t m, const double *
                            const double *params, void *stream);
 
 /*
+ * Alg 5 plus the gradient by-product ("it can compute the Jacobian while
+ * computing the Hessian"): additionally grad[e*n + i] = df/dx_i (points[e]), read from slot
+ * v[1] of row i's evaluations (DEVICE pointer, m x n).  Same other arguments as
+ * chessfad_hessian_batch; ERR_ARG if grad is NULL with m > 0.
+ */
+int chessfad_hessian_grad_batch(int func, int n, int csize, int64_t m, const double *points, double *hess,
+                                double *grad, const double *params, void *stream);
+
+/*
  * Symmetric chunked HVP, Alg 8 SC-HESS-VEC (§III-C): for row
  * i only chunks cn >= i/csize are evaluated (n(n/C+1)/2 evaluations per point);
  * each entry H_is of a chunk strictly after row i's chunk also adds H_is*vecs[i] to out[s].
@@ -151,7 +160,8 @@ enum chessfad_algo {
   CHESSFAD_ALGO_HESSIAN = 1,      /* Alg 5, chessfad_hessian_batch */
   CHESSFAD_ALGO_SYM_HVP = 2,      /* Alg 8, chessfad_sym_hvp_batch */
   CHESSFAD_ALGO_SYM_HESSIAN = 3,  /* Alg 6, chessfad_sym_hessian_batch */
-  CHESSFAD_ALGO_HVP_ROWHOIST = 4  /* Alg 7 + NEXT-4 row-channel hoisting, chessfad_hvp_batch_rowhoist */
+  CHESSFAD_ALGO_HVP_ROWHOIST = 4, /* Alg 7 + NEXT-4 row-channel hoisting, chessfad_hvp_batch_rowhoist */
+  CHESSFAD_ALGO_HESSIAN_GRAD = 5  /* Alg 5 + gradient by-product, chessfad_hessian_grad_batch */
 };
 
 /* 1 if (func, n, csize) runs for the given algorithm, else 0. */

@@ -28,14 +28,21 @@
 
 namespace chessfad {
 
-enum UserAlgo { USER_HVP = MODE_HVP, USER_HESSIAN = MODE_HESS, USER_SYM_HVP = MODE_SYM_HVP, USER_SYM_HESSIAN = MODE_SYM_HESS };
+enum UserAlgo {
+  USER_HVP = MODE_HVP,
+  USER_HESSIAN = MODE_HESS,
+  USER_SYM_HVP = MODE_SYM_HVP,
+  USER_SYM_HESSIAN = MODE_SYM_HESS,
+  USER_HESSIAN_GRAD = MODE_HESS_GRAD
+};
 
 template <int C, int ALGO, class F>
 inline cudaError_t user_batch(const F& f, int n, int64_t m, const double* points, const double* vecs, double* out,
-                              cudaStream_t stream) {
+                              cudaStream_t stream, double* grad = nullptr) {
   if (n < 1 || m < 0 || C < 1 || C > n || n % C != 0 || n > 256) return cudaErrorInvalidValue;
   if (m == 0) return cudaSuccess;
-  if (!points || !out || (!mode_hess(ALGO) && !vecs)) return cudaErrorInvalidValue;
+  if (!points || !out || (!mode_hess(ALGO) && !vecs) || (ALGO == USER_HESSIAN_GRAD && !grad))
+    return cudaErrorInvalidValue;
   if (reg_smem_bytes(uses_trig2pi<F>::value, n, groups_for(n, kWarpsReg, ALGO), ALGO) > 227 * 1024)
     return cudaErrorInvalidValue;
   BatchArgs a;
@@ -47,6 +54,7 @@ inline cudaError_t user_batch(const F& f, int n, int64_t m, const double* points
   a.vecs = vecs;
   a.out = out;
   a.params = nullptr;
+  a.grad = grad;
   return launch_functor<F, C, ALGO>(f, a, stream);
 }
 
@@ -64,6 +72,13 @@ inline cudaError_t user_hessian_batch(const F& f, int n, int64_t m, const double
                                       cudaStream_t stream, bool symmetric = false) {
   return symmetric ? user_batch<C, USER_SYM_HESSIAN>(f, n, m, points, nullptr, hess, stream)
                    : user_batch<C, USER_HESSIAN>(f, n, m, points, nullptr, hess, stream);
+}
+
+// hess as above plus grad[e*n+i] = df/dx_i (points[e])                 (Alg 5 + PAPER.md:252)
+template <int C, class F>
+inline cudaError_t user_hessian_grad_batch(const F& f, int n, int64_t m, const double* points, double* hess,
+                                           double* grad, cudaStream_t stream) {
+  return user_batch<C, USER_HESSIAN_GRAD>(f, n, m, points, nullptr, hess, stream, grad);
 }
 
 }  // namespace chessfad

@@ -18,12 +18,12 @@ ROSENBROCK, ACKLEY, FLETCHER_POWELL, PRODSUM = 0, 1, 2, 3
 FUNCS = {"rosenbrock": ROSENBROCK, "ackley": ACKLEY, "fletcher_powell": FLETCHER_POWELL, "prodsum": PRODSUM}
 STATUS = {0: "CHESSFAD_OK", 1: "CHESSFAD_ERR_ARG", 2: "CHESSFAD_ERR_CHUNK", 3: "CHESSFAD_ERR_FUNC",
           4: "CHESSFAD_ERR_UNSUPPORTED", 5: "CHESSFAD_ERR_CUDA"}
-ALGOS = {"hvp": 0, "hessian": 1, "sym_hvp": 2, "sym_hessian": 3, "hvp_rowhoist": 4}
+ALGOS = {"hvp": 0, "hessian": 1, "sym_hvp": 2, "sym_hessian": 3, "hvp_rowhoist": 4, "hessian_grad": 5}
 EXPORTS = sorted(["chessfad_hvp_batch", "chessfad_hessian_batch", "chessfad_sym_hvp_batch", "chessfad_sym_hessian_batch",
                   "chessfad_hvp_batch_host", "chessfad_is_supported", "chessfad_is_supported_algo",
                   "chessfad_status_string", "chessfad_model_flops_per_point", "chessfad_model_flops_per_point_algo",
                   "chessfad_fp64_probe", "chessfad_version", "chessfad_hvp_host_workspace_bytes",
-                  "chessfad_hvp_batch_rowhoist", "chessfad_hvp_batch_paper_l2"])
+                  "chessfad_hvp_batch_rowhoist", "chessfad_hvp_batch_paper_l2", "chessfad_hessian_grad_batch"])
 
 _lock = threading.Lock()
 _lib = None
@@ -53,6 +53,7 @@ def load(build_if_missing: bool = True):
             "chessfad_hessian_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_sym_hvp_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_hvp_batch_rowhoist": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
+            "chessfad_hessian_grad_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_hvp_batch_paper_l2": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_sym_hessian_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_is_supported_algo": (i32, [i32, i32, i32, i32]),
@@ -155,6 +156,21 @@ def hvp_batch_paper_l2(func, points, vecs, csize: int, out=None, stream=None):
 def hessian_batch(func, points, csize: int, params=None, out=None, stream=None):
     """hess[e] = Hess f(points[e]), every entry computed (Alg 5 CHUNK-HESS, batched): (m, n, n)."""
     return _hess("chessfad_hessian_batch", func, points, csize, params, out, stream)
+
+
+def hessian_grad_batch(func, points, csize: int, params=None, out=None, grad=None, stream=None):
+    """(hess, grad): Alg 5 Hessians plus the gradient by-product from slot v[1]."""
+    import torch
+    m, n = points.shape
+    if out is None:
+        out = torch.empty((m, n, n), dtype=torch.float64, device=points.device)
+    if grad is None:
+        grad = torch.empty((m, n), dtype=torch.float64, device=points.device)
+    st = load().chessfad_hessian_grad_batch(_func(func), n, csize, m, _dev(points, "points"),
+                                            _dev(out, "hess", (m, n, n)), _dev(grad, "grad", (m, n)),
+                                            _dev(params, "params"), _stream_ptr(stream))
+    _check(st)
+    return out, grad
 
 
 def sym_hessian_batch(func, points, csize: int, params=None, out=None, stream=None):

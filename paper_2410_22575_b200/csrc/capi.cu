@@ -108,8 +108,9 @@ cudaError_t dispatch_f3(const BatchArgs& a, cudaStream_t s) {
 
 template <int MODE>
 int run(int func, int n, int csize, int64_t m, const double* points, const double* vecs, double* out,
-        const double* params, cudaStream_t s) {
+        const double* params, cudaStream_t s, double* grad = nullptr) {
   BatchArgs a;
+  a.grad = grad;
   a.n = n;
   a.csize = csize;
   a.groups = 1;
@@ -129,13 +130,14 @@ int run(int func, int n, int csize, int64_t m, const double* points, const doubl
 
 template <int MODE>
 int batch_entry(int func, int n, int csize, int64_t m, const double* points, const double* vecs, double* out,
-                const double* params, void* stream) {
+                const double* params, void* stream, double* grad = nullptr) {
   const bool hess = mode_hess(MODE);
   int st = validate(func, n, csize, m, false, params, points, hess ? out : vecs, out);
   if (st) return st;
+  if (MODE == MODE_HESS_GRAD && m > 0 && !grad) return CHESSFAD_ERR_ARG;
   if (!supported(func, n, csize, MODE)) return CHESSFAD_ERR_UNSUPPORTED;
   if (m == 0) return CHESSFAD_OK;
-  return run<MODE>(func, n, csize, m, points, vecs, out, params, (cudaStream_t)stream);
+  return run<MODE>(func, n, csize, m, points, vecs, out, params, (cudaStream_t)stream, grad);
 }
 
 // ---------------------------------------------------------------- FP64 probe kernel
@@ -171,6 +173,11 @@ int chessfad_sym_hvp_batch(int func, int n, int csize, int64_t m, const double* 
 int chessfad_sym_hessian_batch(int func, int n, int csize, int64_t m, const double* points, double* hess,
                                const double* params, void* stream) {
   return batch_entry<MODE_SYM_HESS>(func, n, csize, m, points, nullptr, hess, params, stream);
+}
+
+int chessfad_hessian_grad_batch(int func, int n, int csize, int64_t m, const double* points, double* hess,
+                                double* grad, const double* params, void* stream) {
+  return batch_entry<MODE_HESS_GRAD>(func, n, csize, m, points, nullptr, hess, params, stream, grad);
 }
 
 int chessfad_hvp_batch_rowhoist(int func, int n, int csize, int64_t m, const double* points, const double* vecs,
@@ -278,11 +285,11 @@ int chessfad_is_supported(int func, int n, int csize) {
 }
 
 int chessfad_is_supported_algo(int func, int n, int csize, int algo) {
-  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_HVP_ROWHOIST) return 0;
+  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_HESSIAN_GRAD) return 0;
   if (validate(func, n, csize, 0, false, func == CHESSFAD_FLETCHER_POWELL ? (const void*)1 : nullptr, nullptr,
                nullptr, nullptr))
     return 0;
-  static const int mode_of[5] = {MODE_HVP, MODE_HESS, MODE_SYM_HVP, MODE_SYM_HESS, MODE_HVP_ROWHOIST};
+  static const int mode_of[6] = {MODE_HVP, MODE_HESS, MODE_SYM_HVP, MODE_SYM_HESS, MODE_HVP_ROWHOIST, MODE_HESS_GRAD};
   return supported(func, n, csize, mode_of[algo]);
 }
 
@@ -299,7 +306,7 @@ const char* chessfad_status_string(int status) {
 }
 
 double chessfad_model_flops_per_point_algo(int func, int n, int csize, int algo) {
-  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_HVP_ROWHOIST) return -1.0;
+  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_HESSIAN_GRAD) return -1.0;
   if (validate(func, n, csize, 0, false, (const void*)1, nullptr, nullptr, nullptr)) return -1.0;
   const double C = csize, N = n;
   // per-evaluation hDual op counts of the canonical forms (DESIGN.md op table)

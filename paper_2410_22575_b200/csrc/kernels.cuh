@@ -33,8 +33,10 @@ namespace chessfad {
 // MODE_HVP_ROWHOIST (NEXT-4, F3 only): Alg 7 with phase A (slots 0/1 of the residuals, which
 // do not depend on the chunk) computed once per row instead of once per chunk; outputs are
 // bit-identical to MODE_HVP, executed FLOPs are below the model count.
-enum { MODE_HVP = 0, MODE_HESS = 1, MODE_SYM_HVP = 2, MODE_SYM_HESS = 3, MODE_HVP_ROWHOIST = 4 };
-__host__ __device__ constexpr bool mode_hess(int M) { return M == MODE_HESS || M == MODE_SYM_HESS; }
+// MODE_HESS_GRAD: Alg 5 plus the gradient by-product df/dx_i = slot v[1] of row i's
+// evaluations (only this mode keeps slot 1 of the result alive).
+enum { MODE_HVP = 0, MODE_HESS = 1, MODE_SYM_HVP = 2, MODE_SYM_HESS = 3, MODE_HVP_ROWHOIST = 4, MODE_HESS_GRAD = 5 };
+__host__ __device__ constexpr bool mode_hess(int M) { return M == MODE_HESS || M == MODE_SYM_HESS || M == MODE_HESS_GRAD; }
 __host__ __device__ constexpr bool mode_sym(int M) { return M == MODE_SYM_HVP || M == MODE_SYM_HESS; }
 
 struct BatchArgs {
@@ -46,6 +48,7 @@ struct BatchArgs {
   const double* __restrict__ vecs;
   double* __restrict__ out;  // HVP: m x n;  Hessian: m x n x n
   const double* __restrict__ params;
+  double* __restrict__ grad;  // MODE_HESS_GRAD: m x n gradient
 };
 
 constexpr int kPad = 33;     // shared-memory row stride (doubles) of [k][lane] tiles
@@ -154,6 +157,7 @@ __global__ void __launch_bounds__(W * 32, CHF_REG_MINB) hvp_reg_kernel(BatchArgs
   for (int i = warp / G; i < n; i += rstep) {
     const int scn = i / Capi;  // row i's first chunk (symmetric modes)
     RowSink<MODE> sink = make_sink<MODE>(p, i, e, v, o);
+    double gi = 0.0;  // MODE_HESS_GRAD: df/dx_i (slot v[1], identical for every chunk of row i)
     for (int j = mode_sym(MODE) ? (scn * Capi) / C : 0; j < nchunk; j++) {
       const int cs = j * C;
       sink.mirror = cs / Capi > scn;
@@ -161,7 +165,9 @@ __global__ void __launch_bounds__(W * 32, CHF_REG_MINB) hvp_reg_kernel(BatchArgs
       const hd<C> t = f.template operator()<C>(n, y);  // CHUNK-INIT + f<hDual<C>>, Alg 7 :389-390
 #pragma unroll
       for (int l = 0; l < C; l++) sink(cs + l, t.v[C + 2 + l]);  // :392-394 / :210-212 / :417-421
+      if (MODE == MODE_HESS_GRAD) gi = t.v[1];
     }
+    if (MODE == MODE_HESS_GRAD && e < p.m) p.grad[e * n + i] = gi;
     if (!HESS) o[i * kPad] = sink.res;
   }
   if (!HESS) {
@@ -242,6 +248,18 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? CHF_F3_SMEM_MINB : 2)
   for (int i = warp / G; i < n; i += rstep) {
     const int scn = i / C;
     RowSink<MODE> sink = make_sink<MODE>(p, i, e, v, o, VEC_TILE ? kPad : 1);
+    if (MODE == MODE_HESS_GRAD && e < p.m) {  // gradient: slot 1 of f = sum_k r_k r_k
+      if (AB_SMEM)
+        f3_phase_a<KB>(n, i, sa, ca, kPad, ABShared{s_ab, n}, Es, R0, R1);
+      else
+        f3_phase_a<KB>(n, i, sa, ca, kPad, ring, Es, R0, R1);
+      double f1 = 0.0;
+      for (int k = 0; k < n; k++) {
+        const double rr1 = R0[k] * R1[k] + R0[k] * R1[k];  // (r*r)[1] = r0 r1 + r0 r1 (Fig. 1)
+        f1 = (k == 0) ? rr1 : f1 + rr1;
+      }
+      p.grad[e * n + i] = f1;
+    }
     if (MODE == MODE_HVP_ROWHOIST) {  // NEXT-4: phase A once per row
       if (AB_SMEM)
         f3_phase_a<KB>(n, i, sa, ca, kPad, ABShared{s_ab, n}, Es, R0, R1);

@@ -81,7 +81,8 @@ cudaError_t launch_f3(BatchArgs a, cudaStream_t s) {
 }
 
 // explicit-instantiation declarations (definitions in inst_*.cu)
-#define CHF_FOR_MODE(X, A, B) X(A, B, MODE_HVP) X(A, B, MODE_HESS) X(A, B, MODE_SYM_HVP) X(A, B, MODE_SYM_HESS)
+#define CHF_FOR_MODE(X, A, B) \
+  X(A, B, MODE_HVP) X(A, B, MODE_HESS) X(A, B, MODE_SYM_HVP) X(A, B, MODE_SYM_HESS) X(A, B, MODE_HESS_GRAD)
 #define CHF_DECL_REG1(F, C, M) extern template cudaError_t launch_reg<F, C, M>(BatchArgs, cudaStream_t);
 #define CHF_DECL_REG(F, C) CHF_FOR_MODE(CHF_DECL_REG1, F, C)
 #define CHF_FOR_C(X, F) X(F, 1) X(F, 2) X(F, 4) X(F, 8) X(F, 16)

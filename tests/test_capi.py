@@ -158,3 +158,13 @@ def test_rowhoist_contract():
     assert not chf.is_supported("rosenbrock", 16, 4, "hvp_rowhoist")
     assert chf.model_flops_per_point("fletcher_powell", 16, 4, algo="hvp_rowhoist") == \
         chf.model_flops_per_point("fletcher_powell", 16, 4)
+
+
+def test_hessian_grad_contract(lib):
+    import paper_2410_22575_b200 as chf
+    assert chf.is_supported("rosenbrock", 16, 4, "hessian_grad")
+    assert chf.model_flops_per_point("ackley", 16, 4, algo="hessian_grad") == \
+        chf.model_flops_per_point("ackley", 16, 4, hessian=True)
+    vp = ctypes.c_void_p
+    # grad NULL with m > 0 -> ERR_ARG, before any CUDA call
+    assert lib.chessfad_hessian_grad_batch(0, 16, 4, 10, vp(1), vp(1), None, None, None) == 1

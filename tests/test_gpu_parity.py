@@ -355,3 +355,32 @@ def test_paper_l2_baseline_parity(chf, func, n):
     for C in divisors(n):
         got = chf.hvp_batch_paper_l2(func, p, v, C).cpu().numpy()
         _check(got, ref, sabs)
+
+
+# ------------------------------------------------------------ gradient by-product
+@pytest.mark.parametrize("func", FUNCS)
+def test_hessian_grad(chf, func):
+    """grad from slot v[1] == the oracle's CHUNK-HESS gradient (and the Hessian is unchanged);
+    Rosenbrock on integer inputs against its exact closed-form gradient, bit for bit."""
+    n, m = 16, 300
+    P = synth.points(19, n, m)
+    params = _params(func, n)
+    dev = torch.device("cuda")
+    p = torch.from_numpy(P).to(dev)
+    pr = None if params is None else torch.from_numpy(params).to(dev)
+    ref_g = np.stack([oracle.hessian(func, P[e], params, algo="chunk", C=4)[1] for e in range(m)])
+    for C in (1, 4, 16):
+        H, g = chf.hessian_grad_batch(func, p, C, pr)
+        H0 = chf.hessian_batch(func, p, C, pr)
+        assert torch.equal(H, H0)
+        g = g.cpu().numpy()
+        scale = np.maximum(np.abs(ref_g).max(axis=1, keepdims=True), 1e-300)
+        assert (np.abs(g - ref_g) / scale).max() <= TIGHT, C
+    if func == "rosenbrock":
+        Pi = synth.int_points(20, n, 64)
+        _, g = chf.hessian_grad_batch(func, torch.from_numpy(Pi).to(dev), 8)
+        a = Pi
+        want = np.zeros_like(a)
+        want[:, :-1] += -400 * a[:, :-1] * (a[:, 1:] - a[:, :-1] ** 2) - 2 * (1 - a[:, :-1])
+        want[:, 1:] += 200 * (a[:, 1:] - a[:, :-1] ** 2)
+        assert np.array_equal(g.cpu().numpy(), want)
