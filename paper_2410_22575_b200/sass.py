@@ -20,8 +20,8 @@ def _tool(name: str) -> str | None:
 
 @functools.lru_cache(maxsize=4)
 def kernel_sass_hashes(lib_path: str) -> dict:
-    """{demangled kernel name: sha256(SASS)[:16]} for every kernel in lib_path ({} if the
-    tools are unavailable)."""
+    """{demangled kernel name: sha256(SASS instruction text)[:16]} for every kernel in
+    lib_path ({} if the tools are unavailable)."""
     cuobjdump, cxxfilt = _tool("cuobjdump"), _tool("c++filt")
     if not cuobjdump or not cxxfilt:
         return {}
@@ -37,7 +37,9 @@ def kernel_sass_hashes(lib_path: str) -> dict:
                 funcs[name] = body
             name, body = m.group(1), []
         elif name and re.match(r"\s+/\*[0-9a-f]{4,}\*/", line):
-            body.append(re.sub(r"/\*[0-9a-f]+\*/", "", line).strip())
+            # instruction text only: drop the address and the encoding word (control bits
+            # such as stall counts can change without changing what executes)
+            body.append(re.sub(r"/\*.*?\*/", "", line).strip())
     if name:
         funcs[name] = body
     mangled = list(funcs)
