@@ -395,7 +395,7 @@ def test_maximum_n(chf):
         m = 3 if func == "fletcher_powell" else 40
         P, V = synth.points(22, n, m), synth.vectors(22, n, m)
         params = _params(func, n)
-        ref, sabs = oracle.hvp_batch(func, P, V, Cs[-1], params)
+        ref, sabs = oracle.hvp_batch(func, P, V, min(Cs[-1], 16 if n > 128 else Cs[-1]), params)  # C-invariant
         for C in Cs:
             assert chf.is_supported(func, n, C)
             _check(_gpu_hvp(chf, func, P, V, C, params), ref, sabs)
