@@ -148,7 +148,7 @@ size_t chessfad_hvp_host_workspace_bytes(int func, int n, int64_t m, int64_t pie
 
 /* 1 if (func, n, csize) runs for both chessfad_hvp_batch and chessfad_hessian_batch, else 0
  * (argument errors also give 0).  Compiled set: Fletcher-
- * Powell any csize | n, n <= 32 or (n <= 128 and n % 8 == 0); the other functions n <= 256 (Ackley n <= 160), with one
+ * Powell any csize | n, n <= 32 or (n <= 128 and n % 8 == 0); the other functions n <= 256 (Ackley n <= 176), with one
  * hDual<csize> per evaluation for csize in {1,2,4,8,16} and, for any other csize | n, csize/c'
  * column groups of the largest c' in {1,2,4,8,16} dividing csize (bit-identical results by
  * slot independence; slots 0/1 recomputed per group). */

@@ -388,9 +388,9 @@ def test_hessian_grad(chf, func):
 
 # ------------------------------------------------------------ maximum sizes of the compiled set
 def test_maximum_n(chf):
-    """Largest n each path accepts: register path n = 256 (Ackley 160),
+    """Largest n each path accepts: register path n = 256 (Ackley 176),
     Fletcher-Powell n = 128; one past the limit is ERR_UNSUPPORTED."""
-    for func, n, Cs in (("rosenbrock", 256, (16, 256)), ("prodsum", 256, (8, 256)), ("ackley", 160, (16, 160)),
+    for func, n, Cs in (("rosenbrock", 256, (16, 256)), ("prodsum", 256, (8, 256)), ("ackley", 176, (16, 176)),
                         ("fletcher_powell", 128, (128,))):
         m = 3 if func == "fletcher_powell" else 40
         P, V = synth.points(22, n, m), synth.vectors(22, n, m)
@@ -400,5 +400,5 @@ def test_maximum_n(chf):
             assert chf.is_supported(func, n, C)
             _check(_gpu_hvp(chf, func, P, V, C, params), ref, sabs)
     assert not chf.is_supported("rosenbrock", 512, 16)
-    assert not chf.is_supported("ackley", 176, 16)
+    assert chf.is_supported("ackley", 176, 16) and not chf.is_supported("ackley", 177, 1)
     assert not chf.is_supported("fletcher_powell", 136, 8)
