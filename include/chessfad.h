@@ -143,6 +143,12 @@ int chessfad_hvp_batch_host(int func, int n, int csize, int64_t m, const double 
 int chessfad_hvp_batch_paper_l2(int func, int n, int csize, int64_t m, const double *points, const double *vecs,
                                 double *out, void *stream);
 
+/* The paper's three GPU levels as comparison baselines: level 0 = Alg 9 L0 (thread per
+ * instance), 1 = Alg 10 L1 (thread per instance x row), 2 = Fig. 2 L2 (= the call above).
+ * Same restrictions; ERR_ARG for another level. */
+int chessfad_hvp_batch_paper(int level, int func, int n, int csize, int64_t m, const double *points,
+                             const double *vecs, double *out, void *stream);
+
 /* Device workspace bytes chessfad_hvp_batch_host needs for (func, n, m, piece_points). */
 size_t chessfad_hvp_host_workspace_bytes(int func, int n, int64_t m, int64_t piece_points);
 

@@ -23,7 +23,8 @@ EXPORTS = sorted(["chessfad_hvp_batch", "chessfad_hessian_batch", "chessfad_sym_
                   "chessfad_hvp_batch_host", "chessfad_is_supported", "chessfad_is_supported_algo",
                   "chessfad_status_string", "chessfad_model_flops_per_point", "chessfad_model_flops_per_point_algo",
                   "chessfad_fp64_probe", "chessfad_version", "chessfad_hvp_host_workspace_bytes",
-                  "chessfad_hvp_batch_rowhoist", "chessfad_hvp_batch_paper_l2", "chessfad_hessian_grad_batch"])
+                  "chessfad_hvp_batch_rowhoist", "chessfad_hvp_batch_paper_l2", "chessfad_hessian_grad_batch",
+                  "chessfad_hvp_batch_paper"])
 
 _lock = threading.Lock()
 _lib = None
@@ -55,6 +56,7 @@ def load(build_if_missing: bool = True):
             "chessfad_hvp_batch_rowhoist": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_hessian_grad_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_hvp_batch_paper_l2": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
+            "chessfad_hvp_batch_paper": (i32, [i32, i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_sym_hessian_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_is_supported_algo": (i32, [i32, i32, i32, i32]),
             "chessfad_model_flops_per_point_algo": (dbl, [i32, i32, i32, i32]),
@@ -149,6 +151,18 @@ def hvp_batch_paper_l2(func, points, vecs, csize: int, out=None, stream=None):
         out = torch.empty_like(points)
     st = load().chessfad_hvp_batch_paper_l2(_func(func), n, csize, m, _dev(points, "points"),
                                             _dev(vecs, "vecs", (m, n)), _dev(out, "out", (m, n)), _stream_ptr(stream))
+    _check(st)
+    return out
+
+
+def hvp_batch_paper(level: int, func, points, vecs, csize: int, out=None, stream=None):
+    """COMPARISON BASELINES: the paper's L0 (Alg 9), L1 (Alg 10) or L2 (Fig. 2) design."""
+    import torch
+    m, n = points.shape
+    if out is None:
+        out = torch.empty_like(points)
+    st = load().chessfad_hvp_batch_paper(level, _func(func), n, csize, m, _dev(points, "points"),
+                                         _dev(vecs, "vecs", (m, n)), _dev(out, "out", (m, n)), _stream_ptr(stream))
     _check(st)
     return out
 

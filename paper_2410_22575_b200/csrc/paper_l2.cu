@@ -1,5 +1,8 @@
-// paper_l2.cu -- the paper's own GPU design, Fig. 2 "L2", recompiled for
-// sm_100a as a MEASURED COMPARISON POINT (not the product path).
+// paper_l2.cu -- the paper's own GPU designs, Alg 9 "L0", Alg 10 "L1"
+// (:459-482) and Fig. 2 "L2" (:485-524), recompiled for sm_100a as MEASURED COMPARISON
+// POINTS (not the product path).  L0: one thread per instance, rows and chunks looped in the
+// thread; L1: one thread per (instance, row), chunks looped; both re-seed the materialised
+// y[NV] per evaluation (:446, :472) and write out once per row (reading G7).
 //
 // As printed: one thread per (instance, row i, chunk j); NETBLK instances per block of
 // NV*NCHUNK threads each; every thread materialises its seed array `hDual<C> y[NV]` with
@@ -61,6 +64,41 @@ __global__ void __launch_bounds__(NETBLK * NV * (NV / C)) paper_l2_kernel(int64_
   }
 }
 
+// L0 (LEVEL 0) and L1 (LEVEL 1): 256-thread blocks, id = blockIdx.x * blockDim.x + threadIdx.x
+template <int FUNC, int NV, int C, int LEVEL>
+__global__ void __launch_bounds__(256) paper_l01_kernel(int64_t m, const double* __restrict__ x,
+                                                        const double* __restrict__ vec, double* __restrict__ out) {
+  constexpr int NCHUNK = NV / C;
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t eid = LEVEL == 0 ? id : id / NV;
+  if (eid >= m) return;
+  const int i0 = LEVEL == 0 ? 0 : (int)(id % NV);
+  const int i1 = LEVEL == 0 ? NV : i0 + 1;
+  hd<C> y[NV];
+  for (int i = i0; i < i1; i++) {
+    double res = 0.0;
+    for (int j = 0; j < NCHUNK; j++) {
+      const int cstart = j * C;
+      for (int k = 0; k < NV; k++) {  // CHUNK-INIT(y, &a[eid*n], n, i, j, csize)
+        y[k].v[0] = x[eid * NV + k];
+        y[k].v[1] = (k == i) ? 1.0 : 0.0;
+        for (int l = 0; l < C; l++) y[k].v[2 + l] = (k - cstart == l) ? 1.0 : 0.0;
+        for (int l = 0; l < C; l++) y[k].v[C + 2 + l] = 0.0;
+      }
+      const hd<C> temp = eval_f<FUNC, C>(NV, ArraySeed<C, NV>{y});
+      for (int l = 0; l < C; l++) res = res + temp.v[C + 2 + l] * vec[eid * NV + cstart + l];
+    }
+    out[eid * NV + i] = res;
+  }
+}
+
+template <int FUNC, int NV, int C, int LEVEL>
+cudaError_t launch_l01(int64_t m, const double* x, const double* v, double* z, cudaStream_t s) {
+  const int64_t threads = LEVEL == 0 ? m : m * NV;
+  paper_l01_kernel<FUNC, NV, C, LEVEL><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(m, x, v, z);
+  return cudaGetLastError();
+}
+
 template <int FUNC, int NV, int C>
 cudaError_t launch_l2(int64_t m, const double* x, const double* v, double* z, cudaStream_t s) {
   constexpr int THREADS_PER_INSTANCE = NV * (NV / C);
@@ -70,25 +108,36 @@ cudaError_t launch_l2(int64_t m, const double* x, const double* v, double* z, cu
   return cudaGetLastError();
 }
 
+template <int FUNC, int NV, int C>
+cudaError_t launch_level(int level, int64_t m, const double* x, const double* v, double* z, cudaStream_t s) {
+  switch (level) {
+    case 0: return launch_l01<FUNC, NV, C, 0>(m, x, v, z, s);
+    case 1: return launch_l01<FUNC, NV, C, 1>(m, x, v, z, s);
+    case 2: return launch_l2<FUNC, NV, C>(m, x, v, z, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 template <int FUNC, int NV>
-cudaError_t dispatch_c(int C, int64_t m, const double* x, const double* v, double* z, cudaStream_t s) {
+cudaError_t dispatch_c(int level, int C, int64_t m, const double* x, const double* v, double* z, cudaStream_t s) {
   switch (C) {
-    case 1: return launch_l2<FUNC, NV, 1>(m, x, v, z, s);
-    case 2: return launch_l2<FUNC, NV, 2>(m, x, v, z, s);
-    case 4: if constexpr (NV >= 4) return launch_l2<FUNC, NV, 4>(m, x, v, z, s); break;
-    case 8: if constexpr (NV >= 8) return launch_l2<FUNC, NV, 8>(m, x, v, z, s); break;
-    case 16: if constexpr (NV >= 16) return launch_l2<FUNC, NV, 16>(m, x, v, z, s); break;
+    case 1: return launch_level<FUNC, NV, 1>(level, m, x, v, z, s);
+    case 2: return launch_level<FUNC, NV, 2>(level, m, x, v, z, s);
+    case 4: if constexpr (NV >= 4) return launch_level<FUNC, NV, 4>(level, m, x, v, z, s); break;
+    case 8: if constexpr (NV >= 8) return launch_level<FUNC, NV, 8>(level, m, x, v, z, s); break;
+    case 16: if constexpr (NV >= 16) return launch_level<FUNC, NV, 16>(level, m, x, v, z, s); break;
   }
   return cudaErrorInvalidValue;
 }
 
 template <int FUNC>
-cudaError_t dispatch_n(int n, int C, int64_t m, const double* x, const double* v, double* z, cudaStream_t s) {
+cudaError_t dispatch_n(int level, int n, int C, int64_t m, const double* x, const double* v, double* z,
+                       cudaStream_t s) {
   switch (n) {
-    case 2: return dispatch_c<FUNC, 2>(C, m, x, v, z, s);
-    case 4: return dispatch_c<FUNC, 4>(C, m, x, v, z, s);
-    case 8: return dispatch_c<FUNC, 8>(C, m, x, v, z, s);
-    case 16: return dispatch_c<FUNC, 16>(C, m, x, v, z, s);
+    case 2: return dispatch_c<FUNC, 2>(level, C, m, x, v, z, s);
+    case 4: return dispatch_c<FUNC, 4>(level, C, m, x, v, z, s);
+    case 8: return dispatch_c<FUNC, 8>(level, C, m, x, v, z, s);
+    case 16: return dispatch_c<FUNC, 16>(level, C, m, x, v, z, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -96,17 +145,23 @@ cudaError_t dispatch_n(int n, int C, int64_t m, const double* x, const double* v
 }  // namespace
 }  // namespace chessfad
 
-extern "C" int chessfad_hvp_batch_paper_l2(int func, int n, int csize, int64_t m, const double* points,
-                                           const double* vecs, double* out, void* stream) {
+extern "C" int chessfad_hvp_batch_paper(int level, int func, int n, int csize, int64_t m, const double* points,
+                                        const double* vecs, double* out, void* stream) {
   using namespace chessfad;
-  if (n < 1 || m < 0) return CHESSFAD_ERR_ARG;
+  if (level < 0 || level > 2 || n < 1 || m < 0) return CHESSFAD_ERR_ARG;
   if (m > 0 && (!points || !vecs || !out)) return CHESSFAD_ERR_ARG;
   if (csize < 1 || csize > n || n % csize) return CHESSFAD_ERR_CHUNK;
   if ((func != CHESSFAD_ROSENBROCK && func != CHESSFAD_PRODSUM) || n < 2) return CHESSFAD_ERR_UNSUPPORTED;
   if (!(n == 2 || n == 4 || n == 8 || n == 16) || csize > 16) return CHESSFAD_ERR_UNSUPPORTED;
   if (m == 0) return CHESSFAD_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  const cudaError_t e = func == CHESSFAD_ROSENBROCK ? dispatch_n<FUNC_ROSENBROCK>(n, csize, m, points, vecs, out, s)
-                                                    : dispatch_n<FUNC_PRODSUM>(n, csize, m, points, vecs, out, s);
+  const cudaError_t e = func == CHESSFAD_ROSENBROCK
+                            ? dispatch_n<FUNC_ROSENBROCK>(level, n, csize, m, points, vecs, out, s)
+                            : dispatch_n<FUNC_PRODSUM>(level, n, csize, m, points, vecs, out, s);
   return e == cudaSuccess ? CHESSFAD_OK : CHESSFAD_ERR_CUDA;
+}
+
+extern "C" int chessfad_hvp_batch_paper_l2(int func, int n, int csize, int64_t m, const double* points,
+                                           const double* vecs, double* out, void* stream) {
+  return chessfad_hvp_batch_paper(2, func, n, csize, m, points, vecs, out, stream);
 }

@@ -355,6 +355,8 @@ def test_paper_l2_baseline_parity(chf, func, n):
     for C in divisors(n):
         got = chf.hvp_batch_paper_l2(func, p, v, C).cpu().numpy()
         _check(got, ref, sabs)
+        for level in (0, 1):
+            _check(chf.hvp_batch_paper(level, func, p, v, C).cpu().numpy(), ref, sabs)
 
 
 # ------------------------------------------------------------ gradient by-product
