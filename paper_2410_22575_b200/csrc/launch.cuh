@@ -11,8 +11,12 @@ constexpr int kWarpsReg = 4;  // register path: 128 threads per CTA (2 CTAs/SM a
 
 // groups of 32 points per CTA so that every warp of the CTA has a row to work on; the
 // symmetric HVP gives every warp its own group (it walks all rows of its points)
+#ifndef CHF_GROUP_ALL_MAXN
+#define CHF_GROUP_ALL_MAXN 8  // warps own whole 32-point groups for n <= 8 (measured +5..23% at n = 4,
+                                  // neutral at 8, -1..35% at n >= 16: profiles/r01/groups/)
+#endif
 inline int groups_for(int n, int warps, int mode) {
-  if (mode == MODE_SYM_HVP) return warps;
+  if (mode == MODE_SYM_HVP || n <= CHF_GROUP_ALL_MAXN) return warps;
   int g = 1;
   while (g * 2 <= warps && n * g * 2 <= warps) g *= 2;
   return g;
