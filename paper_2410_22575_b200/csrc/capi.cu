@@ -73,9 +73,25 @@ int f3_kb(int n) {
   return kb;
 }
 
+template <int F>
+cudaError_t dispatch_small(int C, const BatchArgs& a, cudaStream_t s) {
+#define CHF_SMALL_CASE(FF, CC, NS) \
+  if (C == CC && a.n == NS) return launch_small<FF, CC, NS>(a, s);
+  CHF_FOR_SMALL(CHF_SMALL_CASE, F)
+#undef CHF_SMALL_CASE
+  return cudaErrorInvalidValue;
+}
+
 template <int MODE>
 cudaError_t dispatch_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s) {
   const int C = reg_kernel_chunk(Capi);
+  if (MODE == MODE_HVP && (a.n == 2 || a.n == 4 || a.n == 8)) {  // compile-time small-n kernels
+    switch (func) {
+      case CHESSFAD_ROSENBROCK: return dispatch_small<FUNC_ROSENBROCK>(C, a, s);
+      case CHESSFAD_ACKLEY: return dispatch_small<FUNC_ACKLEY>(C, a, s);
+      case CHESSFAD_PRODSUM: return dispatch_small<FUNC_PRODSUM>(C, a, s);
+    }
+  }
 #define CHF_CASE_C(F)                                  \
   switch (C) {                                         \
     case 1: return launch_reg<F, 1, MODE>(a, s);       \

@@ -176,6 +176,49 @@ __global__ void __launch_bounds__(W * 32, CHF_REG_MINB) hvp_reg_kernel(BatchArgs
   }
 }
 
+// ---------------------------------------------------------------- small n: compile-time NS
+// Alg 7 for n = NS in {2, 4, 8}: one thread per point (the paper's L0 level, Alg 9), the
+// point and vector in registers (vectorised 16-byte loads), every row / chunk / variable loop
+// unrolled at compile time so that the CHUNK-INIT seeds are constants (StaticSeed).  No
+// shared memory and no barrier: at these sizes the tile staging of hvp_reg_kernel costs more
+// than the few evaluations it feeds (profiles/r01/paper_levels/).
+template <class F, int C, int NS>
+__global__ void __launch_bounds__(128) hvp_small_kernel(BatchArgs p, F f) {
+  constexpr bool TRIG = uses_trig2pi<F>::value;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= p.m) return;
+  double a[NS], v[NS], out[NS], ts[NS], tc[NS];
+  const double2* a2 = reinterpret_cast<const double2*>(p.points + e * NS);
+  const double2* v2 = reinterpret_cast<const double2*>(p.vecs + e * NS);
+#pragma unroll
+  for (int q = 0; q < NS / 2; q++) {
+    const double2 x = __ldg(a2 + q), w = __ldg(v2 + q);
+    a[2 * q] = x.x;
+    a[2 * q + 1] = x.y;
+    v[2 * q] = w.x;
+    v[2 * q + 1] = w.y;
+  }
+  if (TRIG) {
+#pragma unroll
+    for (int k = 0; k < NS; k++) sincos(6.283185307179586 * a[k], ts + k, tc + k);
+  }
+#pragma unroll
+  for (int i = 0; i < NS; i++) {
+    double res = 0.0;
+#pragma unroll
+    for (int j = 0; j < NS / C; j++) {
+      const StaticSeed<C> y{a, 1, i, j * C, ts, tc};
+      const hd<C> t = f.template operator()<C>(NS, y);  // CHUNK-INIT + f<hDual<C>>, Alg 7 :389-390
+#pragma unroll
+      for (int l = 0; l < C; l++) res = res + t.v[C + 2 + l] * v[j * C + l];  // :392-394
+    }
+    out[i] = res;
+  }
+  double2* o2 = reinterpret_cast<double2*>(p.out + e * NS);
+#pragma unroll
+  for (int q = 0; q < NS / 2; q++) o2[q] = make_double2(out[2 * q], out[2 * q + 1]);
+}
+
 // ---------------------------------------------------------------- F3 Fletcher-Powell
 // params = [A (n*n) | B (n*n) | E* (n)].  (A_kj, B_kj) are interleaved and transposed,
 // abT[j*n + k], so that the KB k-values of one j are 16-byte broadcast loads at immediate

@@ -84,6 +84,19 @@ cudaError_t launch_f3(BatchArgs a, cudaStream_t s) {
   return e != cudaSuccess ? e : e2;
 }
 
+// small-n HVP (n = NS in {2, 4, 8}): thread per point, compile-time seeds
+template <int FUNC, int C, int NS>
+cudaError_t launch_small(BatchArgs a, cudaStream_t s) {
+  const int grid = (int)((a.m + 127) / 128);
+  hvp_small_kernel<BuiltinFunc<FUNC>, C, NS><<<grid, 128, 0, s>>>(a, BuiltinFunc<FUNC>{});
+  return cudaGetLastError();
+}
+#define CHF_FOR_SMALL(X, F) X(F, 1, 2) X(F, 2, 2) X(F, 1, 4) X(F, 2, 4) X(F, 4, 4) X(F, 1, 8) X(F, 2, 8) X(F, 4, 8) X(F, 8, 8)
+#define CHF_DECL_SMALL(F, C, NS) extern template cudaError_t launch_small<F, C, NS>(BatchArgs, cudaStream_t);
+CHF_FOR_SMALL(CHF_DECL_SMALL, FUNC_ROSENBROCK)
+CHF_FOR_SMALL(CHF_DECL_SMALL, FUNC_ACKLEY)
+CHF_FOR_SMALL(CHF_DECL_SMALL, FUNC_PRODSUM)
+
 // explicit-instantiation declarations (definitions in inst_*.cu)
 #define CHF_FOR_MODE(X, A, B) \
   X(A, B, MODE_HVP) X(A, B, MODE_HESS) X(A, B, MODE_SYM_HVP) X(A, B, MODE_SYM_HESS) X(A, B, MODE_HESS_GRAD)

@@ -21,6 +21,7 @@ enum { FUNC_ROSENBROCK = 0, FUNC_ACKLEY = 1, FUNC_FLETCHER_POWELL = 2, FUNC_PROD
 //   y[k] = < a_k, [k==i], e_{k-cs} if cs <= k < cs+C, 0 ... 0 >          (Alg 4)
 template <int C>
 struct LaneSeed {
+  static constexpr bool kStatic = false;  // runtime n: loops keep their partial unrolling
   const double* a;  // a[k * stride] = coordinate k of this lane's point (shared memory)
   int stride;
   int i, cs;
@@ -41,6 +42,45 @@ struct LaneSeed {
   }
 };
 
+// Compile-time-n seed (small-n path, kernels.cuh hvp_small_kernel): the point lives in
+// registers and every loop over variables, rows and chunks is fully unrolled, so i, cs and
+// k are compile-time constants in each copy and the 0/1 seed slots fold exactly (as in the
+// paper's NV-templated kernels).
+template <int C>
+struct StaticSeed {
+  static constexpr bool kStatic = true;
+  const double* a;  // this thread's point, a[k]
+  int stride;       // 1
+  int i, cs;
+  const double* sin2pi;
+  const double* cos2pi;
+  CHF_INL hd<C> operator()(int k) const {
+    hd<C> y;
+    y.v[0] = a[k];
+    y.v[1] = (k == i) ? 1.0 : 0.0;
+#pragma unroll
+    for (int l = 0; l < C; l++) y.v[2 + l] = (k - cs == l) ? 1.0 : 0.0;
+#pragma unroll
+    for (int l = 0; l < C; l++) y.v[C + 2 + l] = 0.0;
+    return y;
+  }
+};
+
+// Loop over [lo, hi): fully unrolled for a compile-time-n seed, `#pragma unroll UNROLL`
+// otherwise (the runtime-n kernels' schedule is left exactly as it was).
+template <class Seed, int UNROLL, class Body>
+CHF_INL void seed_loop(int lo, int hi, Body&& body) {
+  if constexpr (Seed::kStatic) {
+#pragma unroll
+    for (int k = lo; k < hi; k++) body(k);
+  } else if constexpr (UNROLL > 0) {
+#pragma unroll UNROLL
+    for (int k = lo; k < hi; k++) body(k);
+  } else {
+    for (int k = lo; k < hi; k++) body(k);
+  }
+}
+
 // F1 Rosenbrock: s = sum_{i<n-1} 100 (y_{i+1} - y_i^2)^2 + (1 - y_i)^2
 // per evaluation: 3(n-1) hh*, 3n-4 hh+, n-1 s*, n-1 s+  (DESIGN.md op table)
 template <int C, class Seed>
@@ -52,14 +92,13 @@ CHF_INL hd<C> f_rosenbrock(int n, const Seed& y) {
     const hd<C> e = 1.0 - y0;
     s = 100.0 * (d * d) + e * e;
   }
-#pragma unroll 2
-  for (int i = 1; i < n - 1; i++) {
+  seed_loop<Seed, 2>(1, n - 1, [&](int i) {
     const hd<C> yi = y(i), yi1 = y(i + 1);
     const hd<C> d = yi1 - yi * yi;
     const hd<C> e = 1.0 - yi;
     const hd<C> t = 100.0 * (d * d) + e * e;
     s = s + t;
-  }
+  });
   return s;
 }
 
@@ -73,10 +112,10 @@ CHF_INL hd<C> f_ackley(int n, const Seed& y) {
     const hd<C> y0 = y(0);
     s1 = y0 * y0;
   }
-  for (int i = 1; i < n; i++) {
+  seed_loop<Seed, 0>(1, n, [&](int i) {
     const hd<C> yi = y(i);
     s1 = s1 + yi * yi;
-  }
+  });
   // cos(u), u = 2 pi y_i: (g, g', g'') = (cos u0, -sin u0, -cos u0) with u0 = 2 pi a_i,
   // bit-identical to the tabulated argument (same single rounding of two_pi * a_i)
   auto cos2pi = [&](int k) {
@@ -85,7 +124,7 @@ CHF_INL hd<C> f_ackley(int n, const Seed& y) {
     return hd_unary(u, c, -s, -c);
   };
   hd<C> s2 = cos2pi(0);
-  for (int i = 1; i < n; i++) s2 = s2 + cos2pi(i);
+  seed_loop<Seed, 0>(1, n, [&](int i) { s2 = s2 + cos2pi(i); });
   const double inv_n = 1.0 / n;
   const hd<C> t1 = (-20.0) * exp((-0.2) * sqrt(s1 * inv_n));
   const hd<C> t2 = exp(s2 * inv_n);
@@ -96,8 +135,7 @@ CHF_INL hd<C> f_ackley(int n, const Seed& y) {
 template <int C, class Seed>
 CHF_INL hd<C> f_prodsum(int n, const Seed& y) {
   hd<C> s = y(0) * y(1);
-#pragma unroll 2
-  for (int i = 1; i < n - 1; i++) s = s + y(i) * y(i + 1);
+  seed_loop<Seed, 2>(1, n - 1, [&](int i) { s = s + y(i) * y(i + 1); });
   return s;
 }
 
