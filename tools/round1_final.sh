@@ -7,6 +7,9 @@ rm -f $O/executed_flops.json
 timeout 1500 python -m pytest tests -m gpu -q > $O/final_pytest.log 2>&1; tail -3 $O/final_pytest.log
 # executed-FLOP tables (ncu): counts per point do not depend on m
 bash tools/ncu_executed.sh cfg2 --n 16 --m 1048576
+bash tools/ncu_executed.sh cfg1n2 --n 2 --m 1048576
+bash tools/ncu_executed.sh smalln4 --n 4 --m 1048576
+bash tools/ncu_executed.sh smalln8 --n 8 --m 1048576
 bash tools/ncu_executed.sh cfg2sym --n 16 --m 262144 --algo sym_hvp
 bash tools/ncu_executed.sh cfg2hoist --n 16 --m 262144 --algo hvp_rowhoist --funcs fletcher_powell
 bash tools/ncu_executed.sh cfg4 --n 32 --m 65536 --algo hessian --csizes 1 2 4 8 16 32
@@ -16,6 +19,9 @@ bash tools/ncu_executed.sh cfg3n64f3 --n 64 --m 16384 --funcs fletcher_powell --
 bash tools/ncu_executed.sh cfg3n128 --n 128 --m 65536 --funcs rosenbrock ackley prodsum --csizes 1 2 4 8 16 32 64 128
 bash tools/ncu_executed.sh cfg3n128f3 --n 128 --m 4096 --funcs fletcher_powell --csizes 1 8 32 128
 # event-timed sweeps
+timeout 600 python tools/sweep_bench.py --n 2 --m 1048576 --algo hvp > $O/time_n2.jsonl
+timeout 600 python tools/sweep_bench.py --n 4 --m 1048576 --algo hvp > $O/time_n4.jsonl
+timeout 600 python tools/sweep_bench.py --n 8 --m 1048576 --algo hvp > $O/time_n8.jsonl
 timeout 600 python tools/sweep_bench.py --n 16 --m 1048576 --algo hvp > $O/time_cfg2.jsonl
 timeout 600 python tools/sweep_bench.py --n 16 --m 1048576 --algo sym_hvp > $O/time_cfg2sym.jsonl
 timeout 600 python tools/sweep_bench.py --n 16 --m 1048576 --algo hvp_rowhoist --funcs fletcher_powell > $O/time_cfg2hoist.jsonl
@@ -28,4 +34,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:hvp_reg -c 1 -o $O/prof_headline python tools/profile_sweep.py --funcs rosenbrock --csizes 16 > /dev/null 2>&1
 timeout 600 python bench.py > $O/bench_final.json 2> $O/bench_final.err
 timeout 300 python tools/e2e_probe.py > $O/e2e_probe_final.jsonl 2>&1
+timeout 600 python tools/paper_levels_bench.py > $O/paper_levels_final.jsonl 2>&1
 ls $O
