@@ -85,7 +85,12 @@ cudaError_t dispatch_small(int C, const BatchArgs& a, cudaStream_t s) {
 template <int MODE>
 cudaError_t dispatch_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s) {
   const int C = reg_kernel_chunk(Capi);
-  if (MODE == MODE_HVP && (a.n == 2 || a.n == 4 || a.n == 8)) {  // compile-time small-n kernels
+#ifdef CHF_SMALL16
+  const bool small_n = a.n == 2 || a.n == 4 || a.n == 8 || a.n == 16;
+#else
+  const bool small_n = a.n == 2 || a.n == 4 || a.n == 8;
+#endif
+  if (MODE == MODE_HVP && small_n) {  // compile-time small-n kernels
     switch (func) {
       case CHESSFAD_ROSENBROCK: return dispatch_small<FUNC_ROSENBROCK>(C, a, s);
       case CHESSFAD_ACKLEY: return dispatch_small<FUNC_ACKLEY>(C, a, s);

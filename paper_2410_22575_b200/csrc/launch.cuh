@@ -91,7 +91,13 @@ cudaError_t launch_small(BatchArgs a, cudaStream_t s) {
   hvp_small_kernel<BuiltinFunc<FUNC>, C, NS><<<grid, 128, 0, s>>>(a, BuiltinFunc<FUNC>{});
   return cudaGetLastError();
 }
-#define CHF_FOR_SMALL(X, F) X(F, 1, 2) X(F, 2, 2) X(F, 1, 4) X(F, 2, 4) X(F, 4, 4) X(F, 1, 8) X(F, 2, 8) X(F, 4, 8) X(F, 8, 8)
+#ifdef CHF_SMALL16  // experiment: compile-time path at n = 16
+#define CHF_SMALL16_LIST(X, F) X(F, 1, 16) X(F, 2, 16) X(F, 4, 16) X(F, 8, 16) X(F, 16, 16)
+#else
+#define CHF_SMALL16_LIST(X, F)
+#endif
+#define CHF_FOR_SMALL(X, F) X(F, 1, 2) X(F, 2, 2) X(F, 1, 4) X(F, 2, 4) X(F, 4, 4) X(F, 1, 8) X(F, 2, 8) X(F, 4, 8) X(F, 8, 8) \
+  CHF_SMALL16_LIST(X, F)
 #define CHF_DECL_SMALL(F, C, NS) extern template cudaError_t launch_small<F, C, NS>(BatchArgs, cudaStream_t);
 CHF_FOR_SMALL(CHF_DECL_SMALL, FUNC_ROSENBROCK)
 CHF_FOR_SMALL(CHF_DECL_SMALL, FUNC_ACKLEY)
