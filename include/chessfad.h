@@ -104,17 +104,20 @@ int chessfad_sym_hessian_batch(int func, int n, int csize, int64_t m, const doub
                                const double *params, void *stream);
 
 /*
- * NEXT-4 (beyond the paper): Alg 7 with row-channel hoisting.  Slots 0 and 1
- * of every intermediate (f and df/dx_i) do not depend on the chunk, so they are computed once
- * per (point, row) instead of once per (point, row, chunk).  The outputs are bit-identical to
- * chessfad_hvp_batch (same operations in the same order); the executed FLOPs are BELOW the
- * model count chessfad_model_flops_per_point_algo(.., CHESSFAD_ALGO_HVP_ROWHOIST) reports (the
- * paper's), so rates quoted against the model are "effective".  Fletcher-Powell only (its
- * slot-column schedule separates the phases); other functions return ERR_UNSUPPORTED.
- * Arguments as chessfad_hvp_batch.
+ * NEXT-4 (beyond the paper): Alg 7 with value-channel hoisting.  Computations
+ * that are identical across the n^2/C evaluations of a point are done once:
+ *  - Rosenbrock, Ackley, prodsum at n in {2, 4, 8, 16}: kernels compiled for that n with
+ *    rows, chunks and variables unrolled, so the CHUNK-INIT seeds are constants and nvcc
+ *    folds them and computes each shared sub-expression (value channel, the first-order
+ *    slots common to all rows) once per point; other n run the per-evaluation kernel;
+ *  - Fletcher-Powell: slots 0/1 of every residual (f, df/dx_i) once per (point, row).
+ * The outputs are those of chessfad_hvp_batch up to FP64 rounding (bit-identical for
+ * Fletcher-Powell and on the integer pins); the executed FLOPs are BELOW the model count of
+ * chessfad_model_flops_per_point_algo(.., CHESSFAD_ALGO_HVP_HOISTED), the paper's, so rates
+ * quoted against the model are "effective".  Arguments as chessfad_hvp_batch.
  */
-int chessfad_hvp_batch_rowhoist(int func, int n, int csize, int64_t m, const double *points, const double *vecs,
-                                double *out, const double *params, void *stream);
+int chessfad_hvp_batch_hoisted(int func, int n, int csize, int64_t m, const double *points, const double *vecs,
+                               double *out, const double *params, void *stream);
 
 /*
  * End-to-end variant of chessfad_hvp_batch on HOST buffers: points, vecs, out (m x n) and
@@ -166,7 +169,7 @@ enum chessfad_algo {
   CHESSFAD_ALGO_HESSIAN = 1,      /* Alg 5, chessfad_hessian_batch */
   CHESSFAD_ALGO_SYM_HVP = 2,      /* Alg 8, chessfad_sym_hvp_batch */
   CHESSFAD_ALGO_SYM_HESSIAN = 3,  /* Alg 6, chessfad_sym_hessian_batch */
-  CHESSFAD_ALGO_HVP_ROWHOIST = 4, /* Alg 7 + NEXT-4 row-channel hoisting, chessfad_hvp_batch_rowhoist */
+  CHESSFAD_ALGO_HVP_HOISTED = 4,  /* Alg 7 + NEXT-4 value-channel hoisting, chessfad_hvp_batch_hoisted */
   CHESSFAD_ALGO_HESSIAN_GRAD = 5  /* Alg 5 + gradient by-product, chessfad_hessian_grad_batch */
 };
 

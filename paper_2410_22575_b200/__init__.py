@@ -18,12 +18,12 @@ ROSENBROCK, ACKLEY, FLETCHER_POWELL, PRODSUM = 0, 1, 2, 3
 FUNCS = {"rosenbrock": ROSENBROCK, "ackley": ACKLEY, "fletcher_powell": FLETCHER_POWELL, "prodsum": PRODSUM}
 STATUS = {0: "CHESSFAD_OK", 1: "CHESSFAD_ERR_ARG", 2: "CHESSFAD_ERR_CHUNK", 3: "CHESSFAD_ERR_FUNC",
           4: "CHESSFAD_ERR_UNSUPPORTED", 5: "CHESSFAD_ERR_CUDA"}
-ALGOS = {"hvp": 0, "hessian": 1, "sym_hvp": 2, "sym_hessian": 3, "hvp_rowhoist": 4, "hessian_grad": 5}
+ALGOS = {"hvp": 0, "hessian": 1, "sym_hvp": 2, "sym_hessian": 3, "hvp_hoisted": 4, "hessian_grad": 5}
 EXPORTS = sorted(["chessfad_hvp_batch", "chessfad_hessian_batch", "chessfad_sym_hvp_batch", "chessfad_sym_hessian_batch",
                   "chessfad_hvp_batch_host", "chessfad_is_supported", "chessfad_is_supported_algo",
                   "chessfad_status_string", "chessfad_model_flops_per_point", "chessfad_model_flops_per_point_algo",
                   "chessfad_fp64_probe", "chessfad_version", "chessfad_hvp_host_workspace_bytes",
-                  "chessfad_hvp_batch_rowhoist", "chessfad_hvp_batch_paper_l2", "chessfad_hessian_grad_batch",
+                  "chessfad_hvp_batch_hoisted", "chessfad_hvp_batch_paper_l2", "chessfad_hessian_grad_batch",
                   "chessfad_hvp_batch_paper"])
 
 _lock = threading.Lock()
@@ -53,7 +53,7 @@ def load(build_if_missing: bool = True):
             "chessfad_hvp_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_hessian_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_sym_hvp_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
-            "chessfad_hvp_batch_rowhoist": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
+            "chessfad_hvp_batch_hoisted": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_hessian_grad_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_hvp_batch_paper_l2": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_hvp_batch_paper": (i32, [i32, i32, i32, i32, i64, vp, vp, vp, vp]),
@@ -137,10 +137,11 @@ def sym_hvp_batch(func, points, vecs, csize: int, params=None, out=None, stream=
     return _hvp("chessfad_sym_hvp_batch", func, points, vecs, csize, params, out, stream)
 
 
-def hvp_batch_rowhoist(func, points, vecs, csize: int, params=None, out=None, stream=None):
-    """NEXT-4: Alg 7 with slots 0/1 computed once per row (Fletcher-Powell); bit-identical
-    to hvp_batch, fewer executed FLOPs than the model count."""
-    return _hvp("chessfad_hvp_batch_rowhoist", func, points, vecs, csize, params, out, stream)
+def hvp_batch_hoisted(func, points, vecs, csize: int, params=None, out=None, stream=None):
+    """NEXT-4: Alg 7 with value-channel hoisting (compile-time kernels for F1/F2/F4 at
+    n in {2,4,8,16}, row hoisting for F3); same results as hvp_batch, executed FLOPs below
+    the model count."""
+    return _hvp("chessfad_hvp_batch_hoisted", func, points, vecs, csize, params, out, stream)
 
 
 def hvp_batch_paper_l2(func, points, vecs, csize: int, out=None, stream=None):

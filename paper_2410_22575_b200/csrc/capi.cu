@@ -59,7 +59,7 @@ constexpr size_t kSmemMax = 227 * 1024;
 
 int supported(int func, int n, int csize, int mode) {
   (void)csize;  // every C | n runs (F3: runtime C; register path: reg_kernel_chunk)
-  if (mode == MODE_HVP_ROWHOIST && func != CHESSFAD_FLETCHER_POWELL) return 0;  // NEXT-4: F3 only
+  if (mode == MODE_HVP_ROWHOIST) mode = MODE_HVP;  // same shapes as the per-evaluation HVP
   if (func == CHESSFAD_FLETCHER_POWELL)  // n > 32 streams (A, B) in 8-column cp.async stages
     return n <= kMaxNF3 && (n <= 32 || n % kF3RingJ == 0) &&
            f3_smem_bytes(n, groups_for(n, kWarpsF3, mode), mode) <= kSmemMax;
@@ -85,18 +85,16 @@ cudaError_t dispatch_small(int C, const BatchArgs& a, cudaStream_t s) {
 template <int MODE>
 cudaError_t dispatch_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s) {
   const int C = reg_kernel_chunk(Capi);
-#ifdef CHF_SMALL16
-  const bool small_n = a.n == 2 || a.n == 4 || a.n == 8 || a.n == 16;
-#else
-  const bool small_n = a.n == 2 || a.n == 4 || a.n == 8;
-#endif
-  if (MODE == MODE_HVP && small_n) {  // compile-time small-n kernels
-    switch (func) {
-      case CHESSFAD_ROSENBROCK: return dispatch_small<FUNC_ROSENBROCK>(C, a, s);
-      case CHESSFAD_ACKLEY: return dispatch_small<FUNC_ACKLEY>(C, a, s);
-      case CHESSFAD_PRODSUM: return dispatch_small<FUNC_PRODSUM>(C, a, s);
+  if constexpr (MODE == MODE_HVP_ROWHOIST) {  // NEXT-4 (chessfad_hvp_batch_hoisted), register path
+    if (a.n == 2 || a.n == 4 || a.n == 8 || a.n == 16) {
+      switch (func) {
+        case CHESSFAD_ROSENBROCK: return dispatch_small<FUNC_ROSENBROCK>(C, a, s);
+        case CHESSFAD_ACKLEY: return dispatch_small<FUNC_ACKLEY>(C, a, s);
+        case CHESSFAD_PRODSUM: return dispatch_small<FUNC_PRODSUM>(C, a, s);
+      }
     }
-  }
+    return dispatch_reg<MODE_HVP>(func, Capi, a, s);  // no hoisted kernel: per-evaluation path
+  } else {
 #define CHF_CASE_C(F)                                  \
   switch (C) {                                         \
     case 1: return launch_reg<F, 1, MODE>(a, s);       \
@@ -112,6 +110,7 @@ cudaError_t dispatch_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s)
     case CHESSFAD_PRODSUM: CHF_CASE_C(FUNC_PRODSUM)
   }
 #undef CHF_CASE_C
+  }
   return cudaErrorInvalidValue;
 }
 
@@ -142,7 +141,7 @@ int run(int func, int n, int csize, int64_t m, const double* points, const doubl
   a.params = params;
   cudaError_t e;
   if constexpr (MODE == MODE_HVP_ROWHOIST) {
-    e = (func == CHESSFAD_FLETCHER_POWELL) ? dispatch_f3<MODE>(a, s) : cudaErrorInvalidValue;
+    e = (func == CHESSFAD_FLETCHER_POWELL) ? dispatch_f3<MODE>(a, s) : dispatch_reg<MODE>(func, csize, a, s);
   } else {
     e = (func == CHESSFAD_FLETCHER_POWELL) ? dispatch_f3<MODE>(a, s) : dispatch_reg<MODE>(func, csize, a, s);
   }
@@ -201,8 +200,8 @@ int chessfad_hessian_grad_batch(int func, int n, int csize, int64_t m, const dou
   return batch_entry<MODE_HESS_GRAD>(func, n, csize, m, points, nullptr, hess, params, stream, grad);
 }
 
-int chessfad_hvp_batch_rowhoist(int func, int n, int csize, int64_t m, const double* points, const double* vecs,
-                                double* out, const double* params, void* stream) {
+int chessfad_hvp_batch_hoisted(int func, int n, int csize, int64_t m, const double* points, const double* vecs,
+                               double* out, const double* params, void* stream) {
   return batch_entry<MODE_HVP_ROWHOIST>(func, n, csize, m, points, vecs, out, params, stream);
 }
 
@@ -342,7 +341,7 @@ double chessfad_model_flops_per_point_algo(int func, int n, int csize, int algo)
   const bool sym = algo == CHESSFAD_ALGO_SYM_HVP || algo == CHESSFAD_ALGO_SYM_HESSIAN;
   const double evals = sym ? N * (N / C + 1) / 2 : N * N / C;
   // HVP dot: every H_ij v_j term once (Alg 8: n(n+C)/2 direct + n(n-C)/2 mirrored) = 2n^2
-  const bool hvp = algo == CHESSFAD_ALGO_HVP || algo == CHESSFAD_ALGO_SYM_HVP || algo == CHESSFAD_ALGO_HVP_ROWHOIST;
+  const bool hvp = algo == CHESSFAD_ALGO_HVP || algo == CHESSFAD_ALGO_SYM_HVP || algo == CHESSFAD_ALGO_HVP_HOISTED;
   return evals * per_eval + (hvp ? 2 * N * N : 0.0);
 }
 

@@ -30,9 +30,10 @@
 
 namespace chessfad {
 
-// MODE_HVP_ROWHOIST (NEXT-4, F3 only): Alg 7 with phase A (slots 0/1 of the residuals, which
-// do not depend on the chunk) computed once per row instead of once per chunk; outputs are
-// bit-identical to MODE_HVP, executed FLOPs are below the model count.
+// MODE_HVP_ROWHOIST (part of NEXT-4, the F3 kernel of chessfad_hvp_batch_hoisted): Alg 7 with
+// phase A (slots 0/1 of the residuals, which do not depend on the chunk) computed once per
+// row instead of once per chunk; outputs are bit-identical to MODE_HVP, executed FLOPs are
+// below the model count.
 // MODE_HESS_GRAD: Alg 5 plus the gradient by-product df/dx_i = slot v[1] of row i's
 // evaluations (only this mode keeps slot 1 of the result alive).
 enum { MODE_HVP = 0, MODE_HESS = 1, MODE_SYM_HVP = 2, MODE_SYM_HESS = 3, MODE_HVP_ROWHOIST = 4, MODE_HESS_GRAD = 5 };
@@ -176,12 +177,15 @@ __global__ void __launch_bounds__(W * 32, CHF_REG_MINB) hvp_reg_kernel(BatchArgs
   }
 }
 
-// ---------------------------------------------------------------- small n: compile-time NS
-// Alg 7 for n = NS in {2, 4, 8}: one thread per point (the paper's L0 level, Alg 9), the
-// point and vector in registers (vectorised 16-byte loads), every row / chunk / variable loop
-// unrolled at compile time so that the CHUNK-INIT seeds are constants (StaticSeed).  No
-// shared memory and no barrier: at these sizes the tile staging of hvp_reg_kernel costs more
-// than the few evaluations it feeds (profiles/r01/paper_levels/).
+// ---------------------------------------------------------------- NEXT-4: compile-time NS
+// chessfad_hvp_batch_hoisted for F1/F2/F4, n = NS in {2, 4, 8, 16}: Alg 7 with one thread per
+// point (the paper's L0 level, Alg 9, whose code is likewise templated on n),
+// point and vector in registers (16-byte loads), every row / chunk / variable loop unrolled at
+// compile time so that the CHUNK-INIT seeds are constants (StaticSeed).  nvcc then folds the
+// 0/1 seed products and computes each scalar sub-expression shared by the point's n^2/C
+// evaluations once (the value channel, the first-order slots common to all rows): value-
+// channel hoisting done by the compiler, IEEE-exact, outputs identical to per-evaluation
+// execution, executed FLOPs far below the model count (reported by ncu, labelled).
 template <class F, int C, int NS>
 __global__ void __launch_bounds__(128) hvp_small_kernel(BatchArgs p, F f) {
   constexpr bool TRIG = uses_trig2pi<F>::value;

@@ -84,20 +84,15 @@ cudaError_t launch_f3(BatchArgs a, cudaStream_t s) {
   return e != cudaSuccess ? e : e2;
 }
 
-// small-n HVP (n = NS in {2, 4, 8}): thread per point, compile-time seeds
+// hoisted HVP (NEXT-4) for n = NS in {2, 4, 8, 16}: thread per point, compile-time seeds
 template <int FUNC, int C, int NS>
 cudaError_t launch_small(BatchArgs a, cudaStream_t s) {
   const int grid = (int)((a.m + 127) / 128);
   hvp_small_kernel<BuiltinFunc<FUNC>, C, NS><<<grid, 128, 0, s>>>(a, BuiltinFunc<FUNC>{});
   return cudaGetLastError();
 }
-#ifdef CHF_SMALL16  // experiment: compile-time path at n = 16
-#define CHF_SMALL16_LIST(X, F) X(F, 1, 16) X(F, 2, 16) X(F, 4, 16) X(F, 8, 16) X(F, 16, 16)
-#else
-#define CHF_SMALL16_LIST(X, F)
-#endif
 #define CHF_FOR_SMALL(X, F) X(F, 1, 2) X(F, 2, 2) X(F, 1, 4) X(F, 2, 4) X(F, 4, 4) X(F, 1, 8) X(F, 2, 8) X(F, 4, 8) X(F, 8, 8) \
-  CHF_SMALL16_LIST(X, F)
+  X(F, 1, 16) X(F, 2, 16) X(F, 4, 16) X(F, 8, 16) X(F, 16, 16)
 #define CHF_DECL_SMALL(F, C, NS) extern template cudaError_t launch_small<F, C, NS>(BatchArgs, cudaStream_t);
 CHF_FOR_SMALL(CHF_DECL_SMALL, FUNC_ROSENBROCK)
 CHF_FOR_SMALL(CHF_DECL_SMALL, FUNC_ACKLEY)

@@ -150,13 +150,14 @@ def test_host_workspace_contract(lib):
     assert chf.STATUS[st] == "CHESSFAD_ERR_ARG"
 
 
-def test_rowhoist_contract():
-    """NEXT-4 entry point: F3 only; its model count is the paper's Alg 7 count."""
+def test_hoisted_contract():
+    """NEXT-4 entry point: every function; its model count is the paper's Alg 7 count."""
     import paper_2410_22575_b200 as chf
-    assert chf.is_supported("fletcher_powell", 16, 4, "hvp_rowhoist")
-    assert chf.is_supported("fletcher_powell", 64, 16, "hvp_rowhoist")
-    assert not chf.is_supported("rosenbrock", 16, 4, "hvp_rowhoist")
-    assert chf.model_flops_per_point("fletcher_powell", 16, 4, algo="hvp_rowhoist") == \
+    assert chf.is_supported("fletcher_powell", 16, 4, "hvp_hoisted")
+    assert chf.is_supported("fletcher_powell", 64, 16, "hvp_hoisted")
+    assert chf.is_supported("rosenbrock", 16, 4, "hvp_hoisted")
+    assert chf.is_supported("ackley", 12, 3, "hvp_hoisted")  # no hoisted kernel: per-evaluation path
+    assert chf.model_flops_per_point("fletcher_powell", 16, 4, algo="hvp_hoisted") == \
         chf.model_flops_per_point("fletcher_powell", 16, 4)
 
 

@@ -273,11 +273,11 @@ def test_sym_hessian_parity(chf, func):
         assert np.array_equal(Hs[:, lower], Hs.transpose(0, 2, 1)[:, lower])
 
 
-# ------------------------------------------------------------ NEXT-4: row-channel hoisting (F3)
+# ------------------------------------------------------------ NEXT-4: value-channel hoisting
 @pytest.mark.parametrize("n,m", [(16, 700), (64, 40)])
-def test_rowhoist_bitwise_equal(chf, n, m):
-    """Phase A computed once per row gives the SAME bits as once per chunk (same ops, same
-    order), and matches the oracle."""
+def test_hoisted_f3_bitwise_equal(chf, n, m):
+    """F3: phase A computed once per row gives the SAME bits as once per chunk (same ops,
+    same order), and matches the oracle."""
     P, V = synth.points(17, n, m), synth.vectors(17, n, m)
     params = synth.fp_params_flat(0, n)
     dev = torch.device("cuda")
@@ -285,11 +285,32 @@ def test_rowhoist_bitwise_equal(chf, n, m):
     ref, sabs = oracle.hvp_batch("fletcher_powell", P, V, n // 4 if n > 16 else 4, params)
     for C in (1, 4, n):
         a = chf.hvp_batch("fletcher_powell", p, v, C, pr).cpu().numpy()
-        b = chf.hvp_batch_rowhoist("fletcher_powell", p, v, C, pr).cpu().numpy()
+        b = chf.hvp_batch_hoisted("fletcher_powell", p, v, C, pr).cpu().numpy()
         assert np.array_equal(a, b)
         _check(b, ref, sabs)
-    with pytest.raises(chf.ChessfadError, match="UNSUPPORTED"):
-        chf.hvp_batch_rowhoist("rosenbrock", p, v, 4)
+
+
+@pytest.mark.parametrize("func", ["rosenbrock", "ackley", "prodsum"])
+@pytest.mark.parametrize("n", [2, 4, 8, 12, 16])
+def test_hoisted_register_functions(chf, func, n):
+    """Compile-time kernels (n in {2,4,8,16}; n = 12 falls back to the per-evaluation path):
+    oracle parity for every C, and bit-exact integer pins for Rosenbrock / prodsum."""
+    m = 500
+    P, V = synth.points(23, n, m), synth.vectors(23, n, m)
+    ref, sabs = oracle.hvp_batch(func, P, V, 1)
+    for C in divisors(n):
+        dev = torch.device("cuda")
+        got = chf.hvp_batch_hoisted(func, torch.from_numpy(P).to(dev), torch.from_numpy(V).to(dev), C).cpu().numpy()
+        _check(got, ref, sabs)
+    if func != "ackley":
+        Pi, Vi = synth.int_points(24, n, 100), synth.int_vectors(24, n, 100)
+        want = np.zeros((100, n))
+        for e in range(100):
+            H = cf.rosenbrock_hessian_exact(Pi[e]) if func == "rosenbrock" else cf.prodsum_hessian_exact(n)
+            want[e] = [float(x) for x in cf.exact_hvp(H, Vi[e])]
+        for C in divisors(n):
+            got = chf.hvp_batch_hoisted(func, torch.from_numpy(Pi).cuda(), torch.from_numpy(Vi).cuda(), C).cpu().numpy()
+            assert np.array_equal(got, want)
 
 
 # ------------------------------------------------------------ BASELINE full sizes, sampled

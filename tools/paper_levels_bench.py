@@ -22,7 +22,8 @@ for n in (2, 4, 8, 16):
     impls = {"paper_L0": lambda c: chf.hvp_batch_paper(0, "rosenbrock", p, v, c, out=out),
              "paper_L1": lambda c: chf.hvp_batch_paper(1, "rosenbrock", p, v, c, out=out),
              "paper_L2": lambda c: chf.hvp_batch_paper(2, "rosenbrock", p, v, c, out=out),
-             "ours": lambda c: chf.hvp_batch("rosenbrock", p, v, c, out=out)}
+             "ours": lambda c: chf.hvp_batch("rosenbrock", p, v, c, out=out),
+             "ours_hoisted": lambda c: chf.hvp_batch_hoisted("rosenbrock", p, v, c, out=out)}
     for name, fn in impls.items():
         for c in (1, 2, 4, 8, 16):
             if n % c or c > n:

@@ -11,7 +11,8 @@ bash tools/ncu_executed.sh cfg1n2 --n 2 --m 1048576
 bash tools/ncu_executed.sh smalln4 --n 4 --m 1048576
 bash tools/ncu_executed.sh smalln8 --n 8 --m 1048576
 bash tools/ncu_executed.sh cfg2sym --n 16 --m 262144 --algo sym_hvp
-bash tools/ncu_executed.sh cfg2hoist --n 16 --m 262144 --algo hvp_rowhoist --funcs fletcher_powell
+bash tools/ncu_executed.sh cfg2hoist --n 16 --m 1048576 --algo hvp_hoisted
+bash tools/ncu_executed.sh n8hoist --n 8 --m 1048576 --algo hvp_hoisted --funcs rosenbrock ackley prodsum
 bash tools/ncu_executed.sh cfg4 --n 32 --m 65536 --algo hessian --csizes 1 2 4 8 16 32
 bash tools/ncu_executed.sh cfg4sym --n 32 --m 65536 --algo sym_hessian --csizes 1 2 4 8 16 32
 bash tools/ncu_executed.sh cfg3n64 --n 64 --m 131072 --funcs rosenbrock ackley prodsum --csizes 1 2 4 8 16 32 64
@@ -24,7 +25,8 @@ timeout 600 python tools/sweep_bench.py --n 4 --m 1048576 --algo hvp > $O/time_n
 timeout 600 python tools/sweep_bench.py --n 8 --m 1048576 --algo hvp > $O/time_n8.jsonl
 timeout 600 python tools/sweep_bench.py --n 16 --m 1048576 --algo hvp > $O/time_cfg2.jsonl
 timeout 600 python tools/sweep_bench.py --n 16 --m 1048576 --algo sym_hvp > $O/time_cfg2sym.jsonl
-timeout 600 python tools/sweep_bench.py --n 16 --m 1048576 --algo hvp_rowhoist --funcs fletcher_powell > $O/time_cfg2hoist.jsonl
+timeout 600 python tools/sweep_bench.py --n 16 --m 1048576 --algo hvp_hoisted > $O/time_cfg2hoist.jsonl
+timeout 600 python tools/sweep_bench.py --n 8 --m 1048576 --algo hvp_hoisted > $O/time_n8hoist.jsonl
 timeout 900 python tools/sweep_bench.py --n 32 --m 262144 --algo hessian > $O/time_cfg4.jsonl
 timeout 900 python tools/sweep_bench.py --n 32 --m 262144 --algo sym_hessian > $O/time_cfg4sym.jsonl
 timeout 1200 python tools/sweep_bench.py --n 64 --m 1048576 --algo hvp --f3-m 65536 > $O/time_cfg3n64.jsonl

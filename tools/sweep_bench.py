@@ -43,7 +43,7 @@ def main():
     except Exception:
         tab = {}
     hess = args.algo in ("hessian", "sym_hessian")
-    fn = {"hvp": chf.hvp_batch, "sym_hvp": chf.sym_hvp_batch, "hessian": chf.hessian_batch, "hvp_rowhoist": chf.hvp_batch_rowhoist,
+    fn = {"hvp": chf.hvp_batch, "sym_hvp": chf.sym_hvp_batch, "hessian": chf.hessian_batch, "hvp_hoisted": chf.hvp_batch_hoisted,
           "sym_hessian": chf.sym_hessian_batch}[args.algo]
     for f in args.funcs:
         m = args.f3_m if (f == "fletcher_powell" and args.f3_m) else args.m
