@@ -34,6 +34,7 @@ timeout 1500 python tools/sweep_bench.py --n 128 --m 1048576 --algo hvp --f3-m 8
 # launch list of the bench command and a full capture of the headline kernel
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_bench.csv python bench.py --steps 5 --warmup 3 --no-sweep --no-cpu --e2e-steps 1 > $O/launches_bench_out.json 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:hvp_reg -c 1 -o $O/prof_headline python tools/profile_sweep.py --funcs rosenbrock --csizes 16 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:hvp_small -c 1 -o $O/prof_hoisted16 python tools/profile_sweep.py --funcs rosenbrock --csizes 16 --algo hvp_hoisted > /dev/null 2>&1
 timeout 600 python bench.py > $O/bench_final.json 2> $O/bench_final.err
 timeout 300 python tools/e2e_probe.py > $O/e2e_probe_final.jsonl 2>&1
 timeout 600 python tools/paper_levels_bench.py > $O/paper_levels_final.jsonl 2>&1
