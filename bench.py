@@ -331,7 +331,7 @@ def main():
 
     # ---- the paper's own Fig. 2 L2 kernel design recompiled for sm_100a (comparison baseline)
     paper_l2 = None
-    if chf.is_supported(args.func, n, C) and args.func in ("rosenbrock", "prodsum") and n in (2, 4, 8, 16):
+    if not args.no_sweep and args.func in ("rosenbrock", "prodsum") and n in (2, 4, 8, 16):
         best = None
         for c in (1, 2, 4, 8, 16):
             if n % c:
