@@ -66,6 +66,45 @@ CHF_INL hd<C> operator*(const hd<C>& u, const hd<C>& v) {
   return r;
 }
 
+// Fused accumulate forms (reading R5): acc + u*v, acc - u*v, acc + c*u with every
+// term of the product added onto the running sum one at a time, in the Fig. 1 term order,
+// as one DFMA each.  Per slot these are exactly the multiplications and additions of one
+// hh* (or s*) plus one hh+ (model FLOPs unchanged: 6C+3 mul + 4C+1 add + 2C+2 add =
+// 6C+3 FMAs); only the association of the sum differs from `acc + (u*v)`, i.e. the
+// reduction order of the sum being accumulated.  Used by the built-in test functions
+// (testfuncs.cuh) for their running sums; the plain operators above are unchanged.
+template <int C>
+CHF_INL hd<C> hd_fma(const hd<C>& u, const hd<C>& v, const hd<C>& acc) {
+  hd<C> r;
+  r.v[0] = __fma_rn(u.v[0], v.v[0], acc.v[0]);
+#pragma unroll
+  for (int i = 1; i <= C + 1; i++) r.v[i] = __fma_rn(v.v[0], u.v[i], __fma_rn(u.v[0], v.v[i], acc.v[i]));
+#pragma unroll
+  for (int j = 2; j <= C + 1; j++)
+    r.v[C + j] = __fma_rn(v.v[0], u.v[C + j],
+                          __fma_rn(v.v[1], u.v[j], __fma_rn(u.v[1], v.v[j], __fma_rn(u.v[0], v.v[C + j], acc.v[C + j]))));
+  return r;
+}
+template <int C>
+CHF_INL hd<C> hd_fnma(const hd<C>& u, const hd<C>& v, const hd<C>& acc) {  // acc - u*v
+  hd<C> r;
+  r.v[0] = __fma_rn(-u.v[0], v.v[0], acc.v[0]);
+#pragma unroll
+  for (int i = 1; i <= C + 1; i++) r.v[i] = __fma_rn(-v.v[0], u.v[i], __fma_rn(-u.v[0], v.v[i], acc.v[i]));
+#pragma unroll
+  for (int j = 2; j <= C + 1; j++)
+    r.v[C + j] = __fma_rn(-v.v[0], u.v[C + j],
+                          __fma_rn(-v.v[1], u.v[j], __fma_rn(-u.v[1], v.v[j], __fma_rn(-u.v[0], v.v[C + j], acc.v[C + j]))));
+  return r;
+}
+template <int C>
+CHF_INL hd<C> hd_axpy(double c, const hd<C>& u, const hd<C>& acc) {  // acc + c*u
+  hd<C> r;
+#pragma unroll
+  for (int s = 0; s < hd<C>::N; s++) r.v[s] = __fma_rn(c, u.v[s], acc.v[s]);
+  return r;
+}
+
 // c * u and u * c
 template <int C>
 CHF_INL hd<C> operator*(double c, const hd<C>& u) {
@@ -133,6 +172,19 @@ CHF_INL hd<C> hd_unary(const hd<C>& u, double g0, double g1, double g2) {
   const double g2u1 = g2 * u.v[1];
 #pragma unroll
   for (int k = 2; k <= C + 1; k++) r.v[C + k] = g1 * u.v[C + k] + g2u1 * u.v[k];
+  return r;
+}
+
+// acc + g(u), the unary rule's terms accumulated onto acc (R5, as hd_fma)
+template <int C>
+CHF_INL hd<C> hd_unary_acc(const hd<C>& u, double g0, double g1, double g2, const hd<C>& acc) {
+  hd<C> r;
+  r.v[0] = acc.v[0] + g0;
+#pragma unroll
+  for (int k = 1; k <= C + 1; k++) r.v[k] = __fma_rn(g1, u.v[k], acc.v[k]);
+  const double g2u1 = g2 * u.v[1];
+#pragma unroll
+  for (int k = 2; k <= C + 1; k++) r.v[C + k] = __fma_rn(g2u1, u.v[k], __fma_rn(g1, u.v[C + k], acc.v[C + k]));
   return r;
 }
 

@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(W * 32, CHF_REG_MINB) hvp_reg_kernel(BatchArgs
 // evaluations once (the value channel, the first-order slots common to all rows): value-
 // channel hoisting done by the compiler, IEEE-exact, outputs identical to per-evaluation
 // execution, executed FLOPs far below the model count (reported by ncu, labelled).
-template <class F, int C, int NS>
+template <class F, int C, int NS, bool FUSED>
 __global__ void __launch_bounds__(128) hvp_small_kernel(BatchArgs p, F f) {
   constexpr bool TRIG = uses_trig2pi<F>::value;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(128) hvp_small_kernel(BatchArgs p, F f) {
     double res = 0.0;
 #pragma unroll
     for (int j = 0; j < NS / C; j++) {
-      const StaticSeed<C> y{a, 1, i, j * C, ts, tc};
+      const StaticSeed<C, FUSED> y{a, 1, i, j * C, ts, tc};
       const hd<C> t = f.template operator()<C>(NS, y);  // CHUNK-INIT + f<hDual<C>>, Alg 7 :389-390
 #pragma unroll
       for (int l = 0; l < C; l++) res = res + t.v[C + 2 + l] * v[j * C + l];  // :392-394

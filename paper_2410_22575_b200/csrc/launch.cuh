@@ -85,10 +85,14 @@ cudaError_t launch_f3(BatchArgs a, cudaStream_t s) {
 }
 
 // hoisted HVP (NEXT-4) for n = NS in {2, 4, 8, 16}: thread per point, compile-time seeds
+// Fused accumulate forms (R5) only where they measured faster on this path: Rosenbrock at
+// n = 16, C >= 8 (0.31 vs 0.69 ms: fewer live registers, no spilling); elsewhere the plain
+// forms let nvcc share more across the unrolled evaluations (profiles/r01/fused/).
+constexpr bool small_fused(int FUNC, int C, int NS) { return FUNC == FUNC_ROSENBROCK && NS == 16 && C >= 8; }
 template <int FUNC, int C, int NS>
 cudaError_t launch_small(BatchArgs a, cudaStream_t s) {
   const int grid = (int)((a.m + 127) / 128);
-  hvp_small_kernel<BuiltinFunc<FUNC>, C, NS><<<grid, 128, 0, s>>>(a, BuiltinFunc<FUNC>{});
+  hvp_small_kernel<BuiltinFunc<FUNC>, C, NS, small_fused(FUNC, C, NS)><<<grid, 128, 0, s>>>(a, BuiltinFunc<FUNC>{});
   return cudaGetLastError();
 }
 #define CHF_FOR_SMALL(X, F) X(F, 1, 2) X(F, 2, 2) X(F, 1, 4) X(F, 2, 4) X(F, 4, 4) X(F, 1, 8) X(F, 2, 8) X(F, 4, 8) X(F, 8, 8) \

@@ -25,6 +25,7 @@ namespace {
 template <int C, int NV>
 struct ArraySeed {  // y(k) reads the thread's materialised hDual<C> y[NV]
   static constexpr bool kStatic = false;
+  static constexpr bool kFused = false;  // the paper's design: canonical forms as written
   const hd<C>* y;
   const double* sin2pi = nullptr;  // (unused: built-in Ackley is not offered here)
   const double* cos2pi = nullptr;

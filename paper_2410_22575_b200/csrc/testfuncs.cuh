@@ -22,6 +22,7 @@ enum { FUNC_ROSENBROCK = 0, FUNC_ACKLEY = 1, FUNC_FLETCHER_POWELL = 2, FUNC_PROD
 template <int C>
 struct LaneSeed {
   static constexpr bool kStatic = false;  // runtime n: loops keep their partial unrolling
+  static constexpr bool kFused = true;    // fused accumulate forms (R5) in the running sums
   const double* a;  // a[k * stride] = coordinate k of this lane's point (shared memory)
   int stride;
   int i, cs;
@@ -46,9 +47,13 @@ struct LaneSeed {
 // registers and every loop over variables, rows and chunks is fully unrolled, so i, cs and
 // k are compile-time constants in each copy and the 0/1 seed slots fold exactly (as in the
 // paper's NV-templated kernels).
-template <int C>
+// FUSED: fused accumulate forms (R5) or the plain operators; the plain forms leave nvcc more
+// common subexpressions to share across the unrolled evaluations, which wins for most
+// (F, C, n) of this path (measured, launch.cuh small_fused).
+template <int C, bool FUSED = false>
 struct StaticSeed {
   static constexpr bool kStatic = true;
+  static constexpr bool kFused = FUSED;
   const double* a;  // this thread's point, a[k]
   int stride;       // 1
   int i, cs;
@@ -65,6 +70,11 @@ struct StaticSeed {
     return y;
   }
 };
+
+#ifndef CHF_SUM_UNROLL
+#define CHF_SUM_UNROLL 4  // Rosenbrock term-loop unroll of the runtime-n kernels (measured: 4 > 2 > 1,
+                          // profiles/r01/fused/)
+#endif
 
 // Loop over [lo, hi): fully unrolled for a compile-time-n seed, `#pragma unroll UNROLL`
 // otherwise (the runtime-n kernels' schedule is left exactly as it was).
@@ -83,22 +93,40 @@ CHF_INL void seed_loop(int lo, int hi, Body&& body) {
 
 // F1 Rosenbrock: s = sum_{i<n-1} 100 (y_{i+1} - y_i^2)^2 + (1 - y_i)^2
 // per evaluation: 3(n-1) hh*, 3n-4 hh+, n-1 s*, n-1 s+  (DESIGN.md op table)
+// Running sums use the fused accumulate forms (hdual.cuh, R5): y_{i+1} - y_i*y_i
+// and s + 100 (d*d) + e*e add each product term onto the sum as one DFMA; the same
+// multiplications and additions as the canonical form, reassociated.
 template <int C, class Seed>
 CHF_INL hd<C> f_rosenbrock(int n, const Seed& y) {
   hd<C> s;
-  {
-    const hd<C> y0 = y(0), y1 = y(1);
-    const hd<C> d = y1 - y0 * y0;
-    const hd<C> e = 1.0 - y0;
-    s = 100.0 * (d * d) + e * e;
+  if constexpr (Seed::kFused) {
+    {
+      const hd<C> y0 = y(0), y1 = y(1);
+      const hd<C> d = hd_fnma(y0, y0, y1);
+      const hd<C> e = 1.0 - y0;
+      s = hd_fma(e, e, 100.0 * (d * d));
+    }
+    seed_loop<Seed, CHF_SUM_UNROLL>(1, n - 1, [&](int i) {
+      const hd<C> yi = y(i), yi1 = y(i + 1);
+      const hd<C> d = hd_fnma(yi, yi, yi1);
+      const hd<C> e = 1.0 - yi;
+      s = hd_fma(e, e, hd_axpy(100.0, d * d, s));
+    });
+  } else {  // the canonical form as written (R2)
+    {
+      const hd<C> y0 = y(0), y1 = y(1);
+      const hd<C> d = y1 - y0 * y0;
+      const hd<C> e = 1.0 - y0;
+      s = 100.0 * (d * d) + e * e;
+    }
+    seed_loop<Seed, 2>(1, n - 1, [&](int i) {
+      const hd<C> yi = y(i), yi1 = y(i + 1);
+      const hd<C> d = yi1 - yi * yi;
+      const hd<C> e = 1.0 - yi;
+      const hd<C> t = 100.0 * (d * d) + e * e;
+      s = s + t;
+    });
   }
-  seed_loop<Seed, 2>(1, n - 1, [&](int i) {
-    const hd<C> yi = y(i), yi1 = y(i + 1);
-    const hd<C> d = yi1 - yi * yi;
-    const hd<C> e = 1.0 - yi;
-    const hd<C> t = 100.0 * (d * d) + e * e;
-    s = s + t;
-  });
   return s;
 }
 
@@ -114,7 +142,8 @@ CHF_INL hd<C> f_ackley(int n, const Seed& y) {
   }
   seed_loop<Seed, 0>(1, n, [&](int i) {
     const hd<C> yi = y(i);
-    s1 = s1 + yi * yi;
+    if constexpr (Seed::kFused) s1 = hd_fma(yi, yi, s1);  // s1 + yi*yi, fused (R5)
+    else s1 = s1 + yi * yi;
   });
   // cos(u), u = 2 pi y_i: (g, g', g'') = (cos u0, -sin u0, -cos u0) with u0 = 2 pi a_i,
   // bit-identical to the tabulated argument (same single rounding of two_pi * a_i)
@@ -124,7 +153,14 @@ CHF_INL hd<C> f_ackley(int n, const Seed& y) {
     return hd_unary(u, c, -s, -c);
   };
   hd<C> s2 = cos2pi(0);
-  seed_loop<Seed, 0>(1, n, [&](int i) { s2 = s2 + cos2pi(i); });
+  seed_loop<Seed, 0>(1, n, [&](int i) {
+    if constexpr (Seed::kFused) {  // s2 + cos(2 pi y_i), fused (R5)
+      const hd<C> u = two_pi * y(i);
+      s2 = hd_unary_acc(u, y.cos2pi[i * y.stride], -y.sin2pi[i * y.stride], -y.cos2pi[i * y.stride], s2);
+    } else {
+      s2 = s2 + cos2pi(i);
+    }
+  });
   const double inv_n = 1.0 / n;
   const hd<C> t1 = (-20.0) * exp((-0.2) * sqrt(s1 * inv_n));
   const hd<C> t2 = exp(s2 * inv_n);
@@ -135,7 +171,10 @@ CHF_INL hd<C> f_ackley(int n, const Seed& y) {
 template <int C, class Seed>
 CHF_INL hd<C> f_prodsum(int n, const Seed& y) {
   hd<C> s = y(0) * y(1);
-  seed_loop<Seed, 2>(1, n - 1, [&](int i) { s = s + y(i) * y(i + 1); });
+  seed_loop<Seed, 2>(1, n - 1, [&](int i) {
+    if constexpr (Seed::kFused) s = hd_fma(y(i), y(i + 1), s);  // fused (R5)
+    else s = s + y(i) * y(i + 1);
+  });
   return s;
 }
 
