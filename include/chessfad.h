@@ -120,6 +120,30 @@ int chessfad_hvp_batch_hoisted(int func, int n, int csize, int64_t m, const doub
                                double *out, const double *params, void *stream);
 
 /*
+ * NEXT-4 seed sparsity (beyond the paper), Fletcher-Powell only: Alg 7 with the
+ * terms that multiply an exact zero seed slot skipped.  A CHUNK-INIT seed (Alg 4,
+ * PAPER.md:172-194) has derivative 1 in slot 1 only for variable i and in slot 2+c only for
+ * variable cs+c, so each derivative slot of the E_k sums of F3 has ONE nonzero term; the
+ * value slot does not depend on the seed and is formed once per point.  Work per point
+ * O(n^3) instead of O(n^4/C); every remaining operation is the one the per-evaluation path
+ * performs, in the same order, so with finite inputs `out` equals chessfad_hvp_batch's bit for
+ * bit up to the sign of zero, for every C (C only has to be a valid chunk size).  Executed FLOPs
+ * are far BELOW the model count (CHESSFAD_ALGO_HVP_SEEDSPARSE reports the paper's model);
+ * rates against the model are "effective".  Arguments and errors as chessfad_hvp_batch;
+ * ERR_UNSUPPORTED for the other functions and for n > 128.
+ */
+int chessfad_hvp_batch_seedsparse(int func, int n, int csize, int64_t m, const double *points, const double *vecs,
+                                  double *out, const double *params, void *stream);
+
+/*
+ * The same seed sparsity for the Hessian API (Alg 5 output): hess[e*n*n + i*n + j] as
+ * chessfad_hessian_batch, bit-identical to it up to the sign of zero.  Arguments and errors
+ * as chessfad_hessian_batch; Fletcher-Powell only, n <= 128.
+ */
+int chessfad_hessian_batch_seedsparse(int func, int n, int csize, int64_t m, const double *points, double *hess,
+                                      const double *params, void *stream);
+
+/*
  * End-to-end variant of chessfad_hvp_batch on HOST buffers: points, vecs, out (m x n) and
  * params are HOST pointers (pinned memory gives copy/compute overlap; pageable memory
  * works but serialises).  The batch is split into pieces of `piece_points` points
@@ -170,7 +194,9 @@ enum chessfad_algo {
   CHESSFAD_ALGO_SYM_HVP = 2,      /* Alg 8, chessfad_sym_hvp_batch */
   CHESSFAD_ALGO_SYM_HESSIAN = 3,  /* Alg 6, chessfad_sym_hessian_batch */
   CHESSFAD_ALGO_HVP_HOISTED = 4,  /* Alg 7 + NEXT-4 value-channel hoisting, chessfad_hvp_batch_hoisted */
-  CHESSFAD_ALGO_HESSIAN_GRAD = 5  /* Alg 5 + gradient by-product, chessfad_hessian_grad_batch */
+  CHESSFAD_ALGO_HESSIAN_GRAD = 5, /* Alg 5 + gradient by-product, chessfad_hessian_grad_batch */
+  CHESSFAD_ALGO_HVP_SEEDSPARSE = 6, /* Alg 7 + NEXT-4 seed sparsity (F3), chessfad_hvp_batch_seedsparse */
+  CHESSFAD_ALGO_HESSIAN_SEEDSPARSE = 7 /* Alg 5 + seed sparsity (F3), chessfad_hessian_batch_seedsparse */
 };
 
 /* 1 if (func, n, csize) runs for the given algorithm, else 0. */

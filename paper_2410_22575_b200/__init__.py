@@ -18,12 +18,13 @@ ROSENBROCK, ACKLEY, FLETCHER_POWELL, PRODSUM = 0, 1, 2, 3
 FUNCS = {"rosenbrock": ROSENBROCK, "ackley": ACKLEY, "fletcher_powell": FLETCHER_POWELL, "prodsum": PRODSUM}
 STATUS = {0: "CHESSFAD_OK", 1: "CHESSFAD_ERR_ARG", 2: "CHESSFAD_ERR_CHUNK", 3: "CHESSFAD_ERR_FUNC",
           4: "CHESSFAD_ERR_UNSUPPORTED", 5: "CHESSFAD_ERR_CUDA"}
-ALGOS = {"hvp": 0, "hessian": 1, "sym_hvp": 2, "sym_hessian": 3, "hvp_hoisted": 4, "hessian_grad": 5}
+ALGOS = {"hvp": 0, "hessian": 1, "sym_hvp": 2, "sym_hessian": 3, "hvp_hoisted": 4, "hessian_grad": 5, "hvp_seedsparse": 6,
+         "hessian_seedsparse": 7}
 EXPORTS = sorted(["chessfad_hvp_batch", "chessfad_hessian_batch", "chessfad_sym_hvp_batch", "chessfad_sym_hessian_batch",
                   "chessfad_hvp_batch_host", "chessfad_is_supported", "chessfad_is_supported_algo",
                   "chessfad_status_string", "chessfad_model_flops_per_point", "chessfad_model_flops_per_point_algo",
                   "chessfad_fp64_probe", "chessfad_version", "chessfad_hvp_host_workspace_bytes",
-                  "chessfad_hvp_batch_hoisted", "chessfad_hvp_batch_paper_l2", "chessfad_hessian_grad_batch",
+                  "chessfad_hvp_batch_hoisted", "chessfad_hvp_batch_seedsparse", "chessfad_hessian_batch_seedsparse", "chessfad_hvp_batch_paper_l2", "chessfad_hessian_grad_batch",
                   "chessfad_hvp_batch_paper"])
 
 _lock = threading.Lock()
@@ -54,6 +55,8 @@ def load(build_if_missing: bool = True):
             "chessfad_hessian_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_sym_hvp_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_hvp_batch_hoisted": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
+            "chessfad_hvp_batch_seedsparse": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
+            "chessfad_hessian_batch_seedsparse": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_hessian_grad_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_hvp_batch_paper_l2": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_hvp_batch_paper": (i32, [i32, i32, i32, i32, i64, vp, vp, vp, vp]),
@@ -144,6 +147,12 @@ def hvp_batch_hoisted(func, points, vecs, csize: int, params=None, out=None, str
     return _hvp("chessfad_hvp_batch_hoisted", func, points, vecs, csize, params, out, stream)
 
 
+def hvp_batch_seedsparse(func, points, vecs, csize: int, params=None, out=None, stream=None):
+    """NEXT-4 seed sparsity (Fletcher-Powell): Alg 7 with the products of exact-zero seed slots
+    skipped, O(n^3) per point; equals hvp_batch bit for bit up to the sign of zero."""
+    return _hvp("chessfad_hvp_batch_seedsparse", "chessfad_hessian_batch_seedsparse", func, points, vecs, csize, params, out, stream)
+
+
 def hvp_batch_paper_l2(func, points, vecs, csize: int, out=None, stream=None):
     """COMPARISON BASELINE: the paper's Fig. 2 L2 kernel design recompiled for sm_100a."""
     import torch
@@ -186,6 +195,12 @@ def hessian_grad_batch(func, points, csize: int, params=None, out=None, grad=Non
                                             _dev(params, "params"), _stream_ptr(stream))
     _check(st)
     return out, grad
+
+
+def hessian_batch_seedsparse(func, points, csize: int, params=None, out=None, stream=None):
+    """NEXT-4 seed sparsity for the Hessian API (Fletcher-Powell): equals hessian_batch bit for
+    bit up to the sign of zero, O(n^3) per point."""
+    return _hess("chessfad_hessian_batch_seedsparse", func, points, csize, params, out, stream)
 
 
 def sym_hessian_batch(func, points, csize: int, params=None, out=None, stream=None):

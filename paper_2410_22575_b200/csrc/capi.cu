@@ -66,6 +66,41 @@ int supported(int func, int n, int csize, int mode) {
   return n <= kMaxNReg && reg_smem_bytes(func == CHESSFAD_ACKLEY, n, groups_for(n, kWarpsReg, mode), mode) <= kSmemMax;
 }
 
+// seed-sparse HVP (NEXT-4): Fletcher-Powell only; every C | n gives the same result (the
+// columns of all chunks are formed one by one), so csize only has to be valid
+bool sparse_supported(int func, int n) {
+  return func == CHESSFAD_FLETCHER_POWELL && n <= kMaxNF3 &&
+         f3_sparse_smem_bytes(n, groups_for(n, kWarpsF3, MODE_HVP)) <= kSmemMax;
+}
+
+int f3_kb(int n);
+
+template <bool HESS>
+int sparse_entry(int func, int n, int csize, int64_t m, const double* points, const double* vecs, double* out,
+                 const double* params, void* stream) {
+  int st = validate(func, n, csize, m, false, params, points, HESS ? out : vecs, out);
+  if (st) return st;
+  if (!sparse_supported(func, n)) return CHESSFAD_ERR_UNSUPPORTED;
+  if (m == 0) return CHESSFAD_OK;
+  BatchArgs a{};
+  a.n = n;
+  a.csize = csize;
+  a.groups = 1;
+  a.m = m;
+  a.points = points;
+  a.vecs = vecs;
+  a.out = out;
+  a.params = params;
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (f3_kb(n)) {  // column block: largest power of two <= 16 dividing n
+#define CHF_CASE_SP(CB) \
+  case CB: e = launch_f3_sparse<CB, HESS>(a, (cudaStream_t)stream); break;
+    CHF_FOR_CB(CHF_CASE_SP)
+#undef CHF_CASE_SP
+  }
+  return e == cudaSuccess ? CHESSFAD_OK : CHESSFAD_ERR_CUDA;
+}
+
 // largest power of two <= 16 that divides n: the F3 k-block
 int f3_kb(int n) {
   int kb = 16;
@@ -205,6 +240,16 @@ int chessfad_hvp_batch_hoisted(int func, int n, int csize, int64_t m, const doub
   return batch_entry<MODE_HVP_ROWHOIST>(func, n, csize, m, points, vecs, out, params, stream);
 }
 
+int chessfad_hvp_batch_seedsparse(int func, int n, int csize, int64_t m, const double* points, const double* vecs,
+                                  double* out, const double* params, void* stream) {
+  return sparse_entry<false>(func, n, csize, m, points, vecs, out, params, stream);
+}
+
+int chessfad_hessian_batch_seedsparse(int func, int n, int csize, int64_t m, const double* points, double* hess,
+                                      const double* params, void* stream) {
+  return sparse_entry<true>(func, n, csize, m, points, nullptr, hess, params, stream);
+}
+
 namespace {
 constexpr int kHostSets = 3;  // buffer sets of the host pipeline (pieces in flight)
 int64_t host_piece(int64_t m, int64_t piece_points) {
@@ -305,10 +350,11 @@ int chessfad_is_supported(int func, int n, int csize) {
 }
 
 int chessfad_is_supported_algo(int func, int n, int csize, int algo) {
-  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_HESSIAN_GRAD) return 0;
+  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_HESSIAN_SEEDSPARSE) return 0;
   if (validate(func, n, csize, 0, false, func == CHESSFAD_FLETCHER_POWELL ? (const void*)1 : nullptr, nullptr,
                nullptr, nullptr))
     return 0;
+  if (algo == CHESSFAD_ALGO_HVP_SEEDSPARSE || algo == CHESSFAD_ALGO_HESSIAN_SEEDSPARSE) return sparse_supported(func, n);
   static const int mode_of[6] = {MODE_HVP, MODE_HESS, MODE_SYM_HVP, MODE_SYM_HESS, MODE_HVP_ROWHOIST, MODE_HESS_GRAD};
   return supported(func, n, csize, mode_of[algo]);
 }
@@ -326,7 +372,7 @@ const char* chessfad_status_string(int status) {
 }
 
 double chessfad_model_flops_per_point_algo(int func, int n, int csize, int algo) {
-  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_HESSIAN_GRAD) return -1.0;
+  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_HESSIAN_SEEDSPARSE) return -1.0;
   if (validate(func, n, csize, 0, false, (const void*)1, nullptr, nullptr, nullptr)) return -1.0;
   const double C = csize, N = n;
   // per-evaluation hDual op counts of the canonical forms (DESIGN.md op table)
@@ -341,7 +387,8 @@ double chessfad_model_flops_per_point_algo(int func, int n, int csize, int algo)
   const bool sym = algo == CHESSFAD_ALGO_SYM_HVP || algo == CHESSFAD_ALGO_SYM_HESSIAN;
   const double evals = sym ? N * (N / C + 1) / 2 : N * N / C;
   // HVP dot: every H_ij v_j term once (Alg 8: n(n+C)/2 direct + n(n-C)/2 mirrored) = 2n^2
-  const bool hvp = algo == CHESSFAD_ALGO_HVP || algo == CHESSFAD_ALGO_SYM_HVP || algo == CHESSFAD_ALGO_HVP_HOISTED;
+  const bool hvp = algo == CHESSFAD_ALGO_HVP || algo == CHESSFAD_ALGO_SYM_HVP || algo == CHESSFAD_ALGO_HVP_HOISTED ||
+                   algo == CHESSFAD_ALGO_HVP_SEEDSPARSE;
   return evals * per_eval + (hvp ? 2 * N * N : 0.0);
 }
 

@@ -1,0 +1,182 @@
+// f3_sparse.cuh -- NEXT-4 seed sparsity for F3 Fletcher-Powell: chessfad_hvp_batch_seedsparse.
+//
+// Alg 7 (CHESS-VEC) evaluates f<hDual<C>> on the CHUNK-INIT seeds (Alg 4,
+// PAPER.md:172-194): variable j carries derivative 1 in slot 1 only if j == i (the row) and
+// in slot 2+c only if j == cs+c (the column).  Every other derivative slot of every seed is 0,
+// so in f3.cuh's E_k sums (sum over j of A_kj sin y_j + B_kj cos y_j) all but one term of
+// each derivative slot is a product with an exact zero.  This kernel skips those terms:
+//
+//   slot 0 (value)     E0_k = sum_j A_kj s_j + B_kj c_j          same for every row and column
+//                                                                -> once per point (R0 tile)
+//   slot 1 (row i)     E1_k = fma(B_ki, -s_i, A_ki c_i)          the j = i term of the chain
+//   slot 2+c (col)     E2_k = fma(B_kc, -s_c, A_kc c_c)          the j = col term
+//   slot C+2+c         EC_k = [i == col] fma(B_ki, -c_i, -A_ki s_i)
+//   then, as in f3_phase_b, r = E* - E and d2f/dx_i dx_col = sum_k (r0 rC + r1 r2 + r1 r2 + r0 rC)
+//   (Fig. 1 term order); for col != i, rC = 0 and the r0 rC terms are skipped as well.
+//
+// With finite inputs every skipped term is an exact +-0 added to a nonzero partial, so the
+// result equals chessfad_hvp_batch's bit for bit up to the sign of zero (tested on the GPU);
+// the work per point drops from O(n^4 / C) to O(n^3).  Executed FLOPs are far below the §V
+// model; rates against the model are "effective".
+//
+// Mapping: as hvp_f3_kernel (lane = point, warp = row, CTA = 4 warps sharing a tile).  Per
+// row, columns go in blocks of CB (accumulators and the lane's sin/cos of the block in
+// registers); the inner loop over k reads (A_kj, B_kj) for the block's columns as warp-uniform
+// 16-byte broadcasts from ab[k][j] (interleaved, row-major: contiguous in j), from shared
+// memory for n <= 32 and through the read-only path otherwise.
+#pragma once
+#include "kernels.cuh"
+
+namespace chessfad {
+
+// The j = 0 term of each E chain is written `A x + B y` (f3_fma's FIRST form) and every later
+// term as fma(B, y, fma(A, x, E)); the sparse terms below copy whichever form the full chain
+// used for that j so that nvcc rounds them identically.
+template <bool FIRST>
+CHF_INL double f3_sp_term(double A, double x, double B, double y) {
+  if constexpr (FIRST) return A * x + B * y;
+  else return __fma_rn(B, y, __dmul_rn(A, x));
+}
+
+// one block of CB columns [cb, cb + CB) of row i: fC[q] = d2f/dx_i dx_{cb+q} for col != i
+template <int CB, bool ROW0, bool COL0>
+CHF_INL void f3_sp_block(int n, int i, int cb, double si, double ci, const double2* __restrict__ ab,
+                         const double* __restrict__ sa, const double* __restrict__ ca, double (&fC)[CB]) {
+  double sc[CB], cc[CB];
+#pragma unroll
+  for (int q = 0; q < CB; q++) {
+    sc[q] = sa[(cb + q) * kPad];
+    cc[q] = ca[(cb + q) * kPad];
+  }
+  for (int k = 0; k < n; k++) {
+    const double2 c1 = ab[k * n + i];
+    const double r1 = -f3_sp_term<ROW0>(c1.x, ci, c1.y, -si);  // slot 1: the j = i term
+    const double2* abk = ab + k * n + cb;
+#pragma unroll
+    for (int q = 0; q < CB; q++) {
+      const double2 c = abk[q];
+      const double r2 = (COL0 && q == 0) ? -f3_sp_term<true>(c.x, cc[q], c.y, -sc[q])
+                                         : -f3_sp_term<false>(c.x, cc[q], c.y, -sc[q]);  // slot 2+c
+      const double t = __dmul_rn(r1, r2);
+      const double rr = __fma_rn(r1, r2, t);  // r0 rC + r1 r2 + r1 r2 + r0 rC with rC = 0 (col != i)
+      fC[q] = (k == 0) ? rr : __dadd_rn(fC[q], rr);
+    }
+  }
+}
+
+// row i: out_i = sum_col d2f/dx_i dx_col * v_col, ascending columns (HVP), or the row stored
+// to hrow (HESS; nullptr for ragged-tail lanes)
+template <int CB, bool ROW0, bool HESS>
+CHF_INL double f3_sp_row(int n, int i, const double2* __restrict__ ab, const double* __restrict__ sa,
+                         const double* __restrict__ ca, const double* __restrict__ r0t, const double* __restrict__ v,
+                         int vs, double* __restrict__ hrow) {
+  const double si = sa[i * kPad], ci = ca[i * kPad];
+  // diagonal column: the full slot set (r0, r1 = r2, rC), f3_phase_b's expression
+  double fdiag = 0.0;
+  for (int k = 0; k < n; k++) {
+    const double2 c = ab[k * n + i];
+    const double r0 = r0t[k * kPad];
+    const double r1 = -f3_sp_term<ROW0>(c.x, ci, c.y, -si);
+    const double r2 = r1;
+    const double rC = -f3_sp_term<ROW0>(c.x, -si, c.y, -ci);  // slot C+2+c: sin'' = -sin, cos'' = -cos
+    const double rrC = r0 * rC + r1 * r2 + r1 * r2 + r0 * rC;
+    fdiag = (k == 0) ? rrC : fdiag + rrC;
+  }
+  double res = 0.0;
+  for (int cb = 0; cb < n; cb += CB) {
+    double fC[CB];
+    if (cb == 0) f3_sp_block<CB, ROW0, true>(n, i, cb, si, ci, ab, sa, ca, fC);
+    else f3_sp_block<CB, ROW0, false>(n, i, cb, si, ci, ab, sa, ca, fC);
+#pragma unroll
+    for (int q = 0; q < CB; q++) {
+      const double h = (cb + q == i) ? fdiag : fC[q];
+      if (HESS) {
+        if (hrow) hrow[cb + q] = h;  // a7': H[e][i][col] (Alg 5)
+      } else {
+        res = __fma_rn(h, v[(cb + q) * vs], res);  // a5/a6: ascending columns, as RowSink
+      }
+    }
+  }
+  return res;
+}
+
+// AB_SMEM (n <= 32): (A, B) whole in shared memory, else the interleaved global scratch.
+// SLIM (n > 32): vectors read and outputs written straight from/to global memory (3 tiles).
+// HESS: the Hessian (Alg 5 output, hess[e][i][j]) instead of the HVP.
+template <int CB, bool AB_SMEM, bool SLIM, bool HESS>
+__global__ void __launch_bounds__(kWarpsF3 * 32, 2) hvp_f3_sparse_kernel(BatchArgs p, const double2* __restrict__ ab_g) {
+  extern __shared__ double smem[];
+  const int n = p.n, G = p.groups, P = 32 * G;
+  double* s_sa = smem;                 // [G][n][33]  sin a
+  double* s_ca = s_sa + G * n * kPad;  // [G][n][33]  cos a
+  double* s_r0 = s_ca + G * n * kPad;  // [G][n][33]  r0_k = E*_k - E0_k (slot 0 of the residuals)
+  double* s_vec = s_r0 + G * n * kPad;
+  double* s_out = s_vec + G * n * kPad;
+  double2* s_ab = reinterpret_cast<double2*>(SLIM ? s_vec : s_out + G * n * kPad);
+  const int64_t e0 = (int64_t)blockIdx.x * P;
+  stage_tile(p, e0, P, s_sa, (SLIM || HESS) ? nullptr : s_vec);
+  if (AB_SMEM) {
+    const double* A = p.params;
+    const double* B = p.params + (size_t)n * n;
+    for (int q = threadIdx.x; q < n * n; q += blockDim.x) s_ab[q] = make_double2(A[q], B[q]);  // [k][j]
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < G * n * 32; q += blockDim.x) {
+    const int idx = (q >> 5) * kPad + (q & 31);
+    double s, c;
+    sincos(s_sa[idx], &s, &c);
+    s_sa[idx] = s;
+    s_ca[idx] = c;
+  }
+  __syncthreads();
+  const double2* ab = AB_SMEM ? s_ab : ab_g;
+  const double* Es = p.params + 2 * (size_t)n * n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = warp % G, wg = warp / G, rstep = kWarpsF3 / G;
+  const double* sa = s_sa + g * n * kPad + lane;
+  const double* ca = s_ca + g * n * kPad + lane;
+  double* r0t = s_r0 + g * n * kPad + lane;
+  // slot 0 once per point: E0_k = sum_j (A_kj s_j + B_kj c_j), f3_sum_j's chain with (s, c)
+  for (int k = wg; k < n; k += rstep) {
+    double E;
+    {
+      const double2 c = ab[k * n];
+      E = c.x * sa[0] + c.y * ca[0];
+    }
+    for (int j = 1; j < n; j++) {
+      const double2 c = ab[k * n + j];
+      E = E + c.x * sa[j * kPad] + c.y * ca[j * kPad];
+    }
+    r0t[k * kPad] = Es[k] - E;
+  }
+  __syncthreads();
+
+  const int64_t e = e0 + g * 32 + lane;
+  const int64_t ec = e < p.m ? e : p.m - 1;
+  const double* v = HESS ? nullptr : (SLIM ? p.vecs + ec * n : s_vec + g * n * kPad + lane);
+  const int vs = SLIM ? 1 : kPad;
+  double* o = s_out + g * n * kPad + lane;
+  for (int i = wg; i < n; i += rstep) {
+    double* hrow = (HESS && e < p.m) ? p.out + (e * n + i) * n : nullptr;
+    const double res = (i == 0) ? f3_sp_row<CB, true, HESS>(n, i, ab, sa, ca, r0t, v, vs, hrow)
+                                : f3_sp_row<CB, false, HESS>(n, i, ab, sa, ca, r0t, v, vs, hrow);
+    if (HESS) {
+    } else if (SLIM) {
+      if (e < p.m) p.out[e * n + i] = res;
+    } else {
+      o[i * kPad] = res;
+    }
+  }
+  if (!SLIM && !HESS) {
+    __syncthreads();
+    write_tile(p, e0, P, s_out);
+  }
+}
+
+// (A, B) -> interleaved row-major ab[k * n + j] = (A_kj, B_kj), n > 32
+static __global__ void f3_ab_interleave_kernel(int n, const double* __restrict__ params, double2* __restrict__ ab) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n * n) ab[q] = make_double2(params[q], params[n * n + q]);
+}
+
+}  // namespace chessfad

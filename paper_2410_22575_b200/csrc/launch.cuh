@@ -3,7 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
-#include "kernels.cuh"
+#include "f3_sparse.cuh"  // includes kernels.cuh
 
 namespace chessfad {
 
@@ -83,6 +83,35 @@ cudaError_t launch_f3(BatchArgs a, cudaStream_t s) {
   const cudaError_t e2 = cudaFreeAsync(abT, s);
   return e != cudaSuccess ? e : e2;
 }
+
+// NEXT-4 seed-sparse F3 HVP (f3_sparse.cuh): CB = column block, (A, B) in shared memory for
+// n <= 32, else an interleaved row-major scratch copy; SLIM tiles for n > 32
+inline bool f3_sp_slim(int n) { return n > 32; }
+inline size_t f3_sparse_smem_bytes(int n, int G) {
+  const int tiles = f3_sp_slim(n) ? 3 : 5;
+  return (size_t)tiles * G * n * kPad * sizeof(double) + (f3_ab_smem(n) ? (size_t)n * n * 2 * sizeof(double) : 0);
+}
+template <int CB, bool HESS>
+cudaError_t launch_f3_sparse(BatchArgs a, cudaStream_t s) {
+  a.groups = groups_for(a.n, kWarpsF3, MODE_HVP);
+  const int64_t P = 32 * a.groups;
+  const int grid = (int)((a.m + P - 1) / P);
+  const size_t smem = f3_sparse_smem_bytes(a.n, a.groups);
+  if (f3_ab_smem(a.n))
+    return launch_with_smem(hvp_f3_sparse_kernel<CB, true, false, HESS>, grid, kWarpsF3 * 32, smem, s, a,
+                            (const double2*)nullptr);
+  double2* ab = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&ab, (size_t)a.n * a.n * sizeof(double2), s);
+  if (e != cudaSuccess) return e;
+  f3_ab_interleave_kernel<<<(a.n * a.n + 255) / 256, 256, 0, s>>>(a.n, a.params, ab);
+  e = launch_with_smem(hvp_f3_sparse_kernel<CB, false, true, HESS>, grid, kWarpsF3 * 32, smem, s, a, (const double2*)ab);
+  const cudaError_t e2 = cudaFreeAsync(ab, s);
+  return e != cudaSuccess ? e : e2;
+}
+#define CHF_FOR_CB(X) X(1) X(2) X(4) X(8) X(16)
+#define CHF_DECL_SP(CB) extern template cudaError_t launch_f3_sparse<CB, false>(BatchArgs, cudaStream_t); \
+  extern template cudaError_t launch_f3_sparse<CB, true>(BatchArgs, cudaStream_t);
+CHF_FOR_CB(CHF_DECL_SP)
 
 // hoisted HVP (NEXT-4) for n = NS in {2, 4, 8, 16}: thread per point, compile-time seeds
 // Fused accumulate forms (R5) only where they measured faster on this path: Rosenbrock at

@@ -290,6 +290,44 @@ def test_hoisted_f3_bitwise_equal(chf, n, m):
         _check(b, ref, sabs)
 
 
+@pytest.mark.parametrize("n,m", [(2, 300), (3, 100), (4, 200), (8, 150), (12, 70), (16, 700), (32, 100), (64, 40),
+                                 (128, 33)])
+def test_seedsparse_f3(chf, n, m):
+    """NEXT-4 seed sparsity: skipping the products of exact-zero seed slots leaves the same
+    bits as the per-evaluation path (up to the sign of zero; == treats -0 == +0) for every C,
+    and matches the oracle."""
+    P, V = synth.points(19, n, m), synth.vectors(19, n, m)
+    params = synth.fp_params_flat(0, n)
+    dev = torch.device("cuda")
+    p, v, pr = (torch.from_numpy(x).to(dev) for x in (P, V, params))
+    ms = min(m, 12) if n >= 64 else m  # oracle cost at n = 128: ~3 s per point
+    ref, sabs = oracle.hvp_batch("fletcher_powell", P[:ms], V[:ms], n, params)
+    Cs = sorted({1, n} | ({4} if n % 4 == 0 else set()))
+    for C in Cs:
+        b = chf.hvp_batch_seedsparse("fletcher_powell", p, v, C, pr).cpu().numpy()
+        if n <= 64 or C == n:
+            a = chf.hvp_batch("fletcher_powell", p, v, C, pr).cpu().numpy()
+            assert np.array_equal(a, b), f"C={C}: max |diff| {np.abs(a - b).max():.3e}"
+        _check(b[:ms], ref, sabs)
+
+
+@pytest.mark.parametrize("n,m", [(2, 100), (8, 70), (32, 50), (64, 9)])
+def test_seedsparse_f3_hessian(chf, n, m):
+    """Seed-sparse Hessian (Alg 5 output): same bits as hessian_batch up to the sign of zero,
+    oracle parity."""
+    P = synth.points(21, n, m)
+    params = synth.fp_params_flat(0, n)
+    dev = torch.device("cuda")
+    p, pr = torch.from_numpy(P).to(dev), torch.from_numpy(params).to(dev)
+    Href = oracle.hessian_batch("fletcher_powell", P, n, params)
+    for C in sorted({1, n}):
+        a = chf.hessian_batch("fletcher_powell", p, C, pr).cpu().numpy()
+        b = chf.hessian_batch_seedsparse("fletcher_powell", p, C, pr).cpu().numpy()
+        assert np.array_equal(a, b)
+        rel = np.max(np.abs(b - Href), axis=(1, 2)) / np.max(np.abs(Href), axis=(1, 2))
+        assert rel.max() <= TIGHT
+
+
 @pytest.mark.parametrize("func", ["rosenbrock", "ackley", "prodsum"])
 @pytest.mark.parametrize("n", [2, 4, 8, 12, 16])
 def test_hoisted_register_functions(chf, func, n):
