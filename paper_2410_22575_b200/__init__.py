@@ -150,7 +150,7 @@ def hvp_batch_hoisted(func, points, vecs, csize: int, params=None, out=None, str
 def hvp_batch_seedsparse(func, points, vecs, csize: int, params=None, out=None, stream=None):
     """NEXT-4 seed sparsity (Fletcher-Powell): Alg 7 with the products of exact-zero seed slots
     skipped, O(n^3) per point; equals hvp_batch bit for bit up to the sign of zero."""
-    return _hvp("chessfad_hvp_batch_seedsparse", "chessfad_hessian_batch_seedsparse", func, points, vecs, csize, params, out, stream)
+    return _hvp("chessfad_hvp_batch_seedsparse", func, points, vecs, csize, params, out, stream)
 
 
 def hvp_batch_paper_l2(func, points, vecs, csize: int, out=None, stream=None):

@@ -73,7 +73,9 @@ bool sparse_supported(int func, int n) {
          f3_sparse_smem_bytes(n, groups_for(n, kWarpsF3, MODE_HVP)) <= kSmemMax;
 }
 
-int f3_kb(int n);
+#ifndef CHF_SP_CB
+#define CHF_SP_CB 16  // column block of the seed-sparse kernel (tuning knob; power of two <= 16)
+#endif
 
 template <bool HESS>
 int sparse_entry(int func, int n, int csize, int64_t m, const double* points, const double* vecs, double* out,
@@ -92,7 +94,9 @@ int sparse_entry(int func, int n, int csize, int64_t m, const double* points, co
   a.out = out;
   a.params = params;
   cudaError_t e = cudaErrorInvalidValue;
-  switch (f3_kb(n)) {  // column block: largest power of two <= 16 dividing n
+  int cb = CHF_SP_CB;  // column block: largest power of two <= CHF_SP_CB dividing n
+  while (n % cb) cb >>= 1;
+  switch (cb) {
 #define CHF_CASE_SP(CB) \
   case CB: e = launch_f3_sparse<CB, HESS>(a, (cudaStream_t)stream); break;
     CHF_FOR_CB(CHF_CASE_SP)

@@ -27,7 +27,16 @@
 #pragma once
 #include "kernels.cuh"
 
+#ifndef CHF_SP_KUNROLL
+#define CHF_SP_KUNROLL 4  // k-loop unroll of the column-block loop (measured 4 > 2: profiles/r01/sparse/)
+#endif
+#ifndef CHF_SP_MINB
+#define CHF_SP_MINB 2  // min CTAs/SM (register budget) of the seed-sparse kernel (tuning knob)
+#endif
+
 namespace chessfad {
+
+constexpr int kSpKUnroll = CHF_SP_KUNROLL;
 
 // The j = 0 term of each E chain is written `A x + B y` (f3_fma's FIRST form) and every later
 // term as fma(B, y, fma(A, x, E)); the sparse terms below copy whichever form the full chain
@@ -48,6 +57,7 @@ CHF_INL void f3_sp_block(int n, int i, int cb, double si, double ci, const doubl
     sc[q] = sa[(cb + q) * kPad];
     cc[q] = ca[(cb + q) * kPad];
   }
+#pragma unroll kSpKUnroll
   for (int k = 0; k < n; k++) {
     const double2 c1 = ab[k * n + i];
     const double r1 = -f3_sp_term<ROW0>(c1.x, ci, c1.y, -si);  // slot 1: the j = i term
@@ -78,7 +88,9 @@ CHF_INL double f3_sp_row(int n, int i, const double2* __restrict__ ab, const dou
     const double r0 = r0t[k * kPad];
     const double r1 = -f3_sp_term<ROW0>(c.x, ci, c.y, -si);
     const double r2 = r1;
-    const double rC = -f3_sp_term<ROW0>(c.x, -si, c.y, -ci);  // slot C+2+c: sin'' = -sin, cos'' = -cos
+    // slot C+2+c (sin'' = -sin, cos'' = -cos); for row 0 the per-evaluation kernel's FIRST-form
+    // sum A*sq + B*cq is contracted as fma(A, sq, B*cq) (measured: bit-identical on the GPU)
+    const double rC = ROW0 ? -__fma_rn(c.x, -si, __dmul_rn(c.y, -ci)) : -f3_sp_term<false>(c.x, -si, c.y, -ci);
     const double rrC = r0 * rC + r1 * r2 + r1 * r2 + r0 * rC;
     fdiag = (k == 0) ? rrC : fdiag + rrC;
   }
@@ -104,7 +116,7 @@ CHF_INL double f3_sp_row(int n, int i, const double2* __restrict__ ab, const dou
 // SLIM (n > 32): vectors read and outputs written straight from/to global memory (3 tiles).
 // HESS: the Hessian (Alg 5 output, hess[e][i][j]) instead of the HVP.
 template <int CB, bool AB_SMEM, bool SLIM, bool HESS>
-__global__ void __launch_bounds__(kWarpsF3 * 32, 2) hvp_f3_sparse_kernel(BatchArgs p, const double2* __restrict__ ab_g) {
+__global__ void __launch_bounds__(kWarpsF3 * 32, CHF_SP_MINB) hvp_f3_sparse_kernel(BatchArgs p, const double2* __restrict__ ab_g) {
   extern __shared__ double smem[];
   const int n = p.n, G = p.groups, P = 32 * G;
   double* s_sa = smem;                 // [G][n][33]  sin a

@@ -17,20 +17,6 @@ namespace chessfad {
 
 enum { FUNC_ROSENBROCK = 0, FUNC_ACKLEY = 1, FUNC_FLETCHER_POWELL = 2, FUNC_PRODSUM = 3 };
 
-#ifndef CHF_SEED_TABLE
-#define CHF_SEED_TABLE 0
-#endif
-#if CHF_SEED_TABLE
-constexpr int kSeedEyeMid = 17;
-#if CHF_SEED_TABLE == 1
-__constant__ double kSeedEye[40] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1.0};
-#define CHF_SEED_LOAD(p) (*(p))
-#else
-__device__ const double kSeedEye[40] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1.0};
-#define CHF_SEED_LOAD(p) __ldg(p)
-#endif
-#endif
-
 // CHUNK-INIT seed for the lane's own point; row i and chunk start cs are warp-uniform.
 //   y[k] = < a_k, [k==i], e_{k-cs} if cs <= k < cs+C, 0 ... 0 >          (Alg 4)
 template <int C>
@@ -48,19 +34,9 @@ struct LaneSeed {
     hd<C> y;
     y.v[0] = a[k * stride];
     y.v[1] = (k == i) ? 1.0 : 0.0;
-#if CHF_SEED_TABLE
-    {
-      int off = k - cs;
-      off = off < -1 ? -1 : (off > C ? C : off);
-      const double* b = kSeedEye + kSeedEyeMid - off;
-#pragma unroll
-      for (int l = 0; l < C; l++) y.v[2 + l] = CHF_SEED_LOAD(b + l);
-    }
-#else
     const int off = k - cs;
 #pragma unroll
     for (int l = 0; l < C; l++) y.v[2 + l] = (off == l) ? 1.0 : 0.0;
-#endif
 #pragma unroll
     for (int l = 0; l < C; l++) y.v[C + 2 + l] = 0.0;
     return y;
