@@ -74,12 +74,69 @@ CHF_INL void f3_sp_block(int n, int i, int cb, double si, double ci, const doubl
   }
 }
 
+// n > 32, n % kSpKS == 0: the block's (A, B) rows ab[k][cb .. cb+CB) do not depend on the row
+// i, so the CTA's 4 warps (which walk the same (cb, k) sequence for their different rows) share
+// them through a cp.async double buffer of kSpKS k-values in shared memory; each warp's own
+// column ab[k][i] (slot 1) rides in a per-warp buffer of the same stages.  Replaces the
+// latency-bound broadcast loads from L2 ((A, B) is 256 KB at n = 128).
+constexpr int kSpKS = 8;
+struct SpRing {
+  double2* blk;  // [2][kSpKS][CB], CTA-shared
+  double2* col;  // [2][kSpKS], this warp's
+};
+
+template <int CB, bool ROW0, bool COL0>
+CHF_INL void f3_sp_block_staged(int n, int i, int cb, double si, double ci, const double2* __restrict__ ab,
+                                const SpRing& rg, const double* __restrict__ sa, const double* __restrict__ ca,
+                                double (&fC)[CB]) {
+  double sc[CB], cc[CB];
+#pragma unroll
+  for (int q = 0; q < CB; q++) {
+    sc[q] = sa[(cb + q) * kPad];
+    cc[q] = ca[(cb + q) * kPad];
+  }
+  const int S = n / kSpKS, lane = threadIdx.x & 31;
+  auto issue = [&](int st) {
+    const int k0 = st * kSpKS, buf = st & 1;
+    for (int q = threadIdx.x; q < kSpKS * CB; q += blockDim.x) {
+      const int kk = q / CB, cq = q - kk * CB;
+      cp_async16(rg.blk + (buf * kSpKS + kk) * CB + cq, ab + (size_t)(k0 + kk) * n + cb + cq);
+    }
+    if (lane < kSpKS) cp_async16(rg.col + buf * kSpKS + lane, ab + (size_t)(k0 + lane) * n + i);
+    cp_async_commit();
+  };
+  __syncthreads();  // every warp is done with the previous block's buffers
+  issue(0);
+  for (int st = 0; st < S; st++) {
+    cp_async_wait<0>();
+    __syncthreads();  // stage st landed for all threads; stage st-1's buffer is free
+    if (st + 1 < S) issue(st + 1);
+    const double2* blk = rg.blk + (st & 1) * kSpKS * CB;
+    const double2* col = rg.col + (st & 1) * kSpKS;
+#pragma unroll
+    for (int kk = 0; kk < kSpKS; kk++) {
+      const int k = st * kSpKS + kk;
+      const double2 c1 = col[kk];
+      const double r1 = -f3_sp_term<ROW0>(c1.x, ci, c1.y, -si);
+#pragma unroll
+      for (int q = 0; q < CB; q++) {
+        const double2 c = blk[kk * CB + q];
+        const double r2 = (COL0 && q == 0) ? -f3_sp_term<true>(c.x, cc[q], c.y, -sc[q])
+                                           : -f3_sp_term<false>(c.x, cc[q], c.y, -sc[q]);
+        const double t = __dmul_rn(r1, r2);
+        const double rr = __fma_rn(r1, r2, t);
+        fC[q] = (k == 0) ? rr : __dadd_rn(fC[q], rr);
+      }
+    }
+  }
+}
+
 // row i: out_i = sum_col d2f/dx_i dx_col * v_col, ascending columns (HVP), or the row stored
 // to hrow (HESS; nullptr for ragged-tail lanes)
-template <int CB, bool ROW0, bool HESS>
+template <int CB, bool ROW0, bool HESS, bool STAGED>
 CHF_INL double f3_sp_row(int n, int i, const double2* __restrict__ ab, const double* __restrict__ sa,
                          const double* __restrict__ ca, const double* __restrict__ r0t, const double* __restrict__ v,
-                         int vs, double* __restrict__ hrow) {
+                         int vs, double* __restrict__ hrow, const SpRing& rg) {
   const double si = sa[i * kPad], ci = ca[i * kPad];
   // diagonal column: the full slot set (r0, r1 = r2, rC), f3_phase_b's expression
   double fdiag = 0.0;
@@ -97,8 +154,13 @@ CHF_INL double f3_sp_row(int n, int i, const double2* __restrict__ ab, const dou
   double res = 0.0;
   for (int cb = 0; cb < n; cb += CB) {
     double fC[CB];
-    if (cb == 0) f3_sp_block<CB, ROW0, true>(n, i, cb, si, ci, ab, sa, ca, fC);
-    else f3_sp_block<CB, ROW0, false>(n, i, cb, si, ci, ab, sa, ca, fC);
+    if constexpr (STAGED) {
+      if (cb == 0) f3_sp_block_staged<CB, ROW0, true>(n, i, cb, si, ci, ab, rg, sa, ca, fC);
+      else f3_sp_block_staged<CB, ROW0, false>(n, i, cb, si, ci, ab, rg, sa, ca, fC);
+    } else {
+      if (cb == 0) f3_sp_block<CB, ROW0, true>(n, i, cb, si, ci, ab, sa, ca, fC);
+      else f3_sp_block<CB, ROW0, false>(n, i, cb, si, ci, ab, sa, ca, fC);
+    }
 #pragma unroll
     for (int q = 0; q < CB; q++) {
       const double h = (cb + q == i) ? fdiag : fC[q];
@@ -115,7 +177,9 @@ CHF_INL double f3_sp_row(int n, int i, const double2* __restrict__ ab, const dou
 // AB_SMEM (n <= 32): (A, B) whole in shared memory, else the interleaved global scratch.
 // SLIM (n > 32): vectors read and outputs written straight from/to global memory (3 tiles).
 // HESS: the Hessian (Alg 5 output, hess[e][i][j]) instead of the HVP.
-template <int CB, bool AB_SMEM, bool SLIM, bool HESS>
+// STAGED (SLIM, n % kSpKS == 0): the CTA-shared (A, B) block rows go through the cp.async
+// double buffer (f3_sp_block_staged); every warp then has n / 4 rows (uniform barriers).
+template <int CB, bool AB_SMEM, bool SLIM, bool HESS, bool STAGED>
 __global__ void __launch_bounds__(kWarpsF3 * 32, CHF_SP_MINB) hvp_f3_sparse_kernel(BatchArgs p, const double2* __restrict__ ab_g) {
   extern __shared__ double smem[];
   const int n = p.n, G = p.groups, P = 32 * G;
@@ -168,10 +232,12 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, CHF_SP_MINB) hvp_f3_sparse_kern
   const double* v = HESS ? nullptr : (SLIM ? p.vecs + ec * n : s_vec + g * n * kPad + lane);
   const int vs = SLIM ? 1 : kPad;
   double* o = s_out + g * n * kPad + lane;
+  // STAGED ring: [2][kSpKS][CB] shared block rows, then [warps][2][kSpKS] column values
+  const SpRing rg{s_ab, s_ab + 2 * kSpKS * CB + warp * 2 * kSpKS};
   for (int i = wg; i < n; i += rstep) {
     double* hrow = (HESS && e < p.m) ? p.out + (e * n + i) * n : nullptr;
-    const double res = (i == 0) ? f3_sp_row<CB, true, HESS>(n, i, ab, sa, ca, r0t, v, vs, hrow)
-                                : f3_sp_row<CB, false, HESS>(n, i, ab, sa, ca, r0t, v, vs, hrow);
+    const double res = (i == 0) ? f3_sp_row<CB, true, HESS, STAGED>(n, i, ab, sa, ca, r0t, v, vs, hrow, rg)
+                                : f3_sp_row<CB, false, HESS, STAGED>(n, i, ab, sa, ca, r0t, v, vs, hrow, rg);
     if (HESS) {
     } else if (SLIM) {
       if (e < p.m) p.out[e * n + i] = res;

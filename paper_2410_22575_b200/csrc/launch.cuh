@@ -87,9 +87,12 @@ cudaError_t launch_f3(BatchArgs a, cudaStream_t s) {
 // NEXT-4 seed-sparse F3 HVP (f3_sparse.cuh): CB = column block, (A, B) in shared memory for
 // n <= 32, else an interleaved row-major scratch copy; SLIM tiles for n > 32
 inline bool f3_sp_slim(int n) { return n > 32; }
+inline bool f3_sp_staged(int n) { return f3_sp_slim(n) && n % kSpKS == 0; }
 inline size_t f3_sparse_smem_bytes(int n, int G) {
   const int tiles = f3_sp_slim(n) ? 3 : 5;
-  return (size_t)tiles * G * n * kPad * sizeof(double) + (f3_ab_smem(n) ? (size_t)n * n * 2 * sizeof(double) : 0);
+  const size_t ring = (size_t)(2 * kSpKS * 16 + kWarpsF3 * 2 * kSpKS) * 2 * sizeof(double);  // STAGED, CB <= 16
+  return (size_t)tiles * G * n * kPad * sizeof(double) + (f3_ab_smem(n) ? (size_t)n * n * 2 * sizeof(double) : 0) +
+         (f3_sp_staged(n) ? ring : 0);
 }
 template <int CB, bool HESS>
 cudaError_t launch_f3_sparse(BatchArgs a, cudaStream_t s) {
@@ -98,13 +101,17 @@ cudaError_t launch_f3_sparse(BatchArgs a, cudaStream_t s) {
   const int grid = (int)((a.m + P - 1) / P);
   const size_t smem = f3_sparse_smem_bytes(a.n, a.groups);
   if (f3_ab_smem(a.n))
-    return launch_with_smem(hvp_f3_sparse_kernel<CB, true, false, HESS>, grid, kWarpsF3 * 32, smem, s, a,
+    return launch_with_smem(hvp_f3_sparse_kernel<CB, true, false, HESS, false>, grid, kWarpsF3 * 32, smem, s, a,
                             (const double2*)nullptr);
   double2* ab = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&ab, (size_t)a.n * a.n * sizeof(double2), s);
   if (e != cudaSuccess) return e;
   f3_ab_interleave_kernel<<<(a.n * a.n + 255) / 256, 256, 0, s>>>(a.n, a.params, ab);
-  e = launch_with_smem(hvp_f3_sparse_kernel<CB, false, true, HESS>, grid, kWarpsF3 * 32, smem, s, a, (const double2*)ab);
+  e = f3_sp_staged(a.n)
+          ? launch_with_smem(hvp_f3_sparse_kernel<CB, false, true, HESS, true>, grid, kWarpsF3 * 32, smem, s, a,
+                             (const double2*)ab)
+          : launch_with_smem(hvp_f3_sparse_kernel<CB, false, true, HESS, false>, grid, kWarpsF3 * 32, smem, s, a,
+                             (const double2*)ab);
   const cudaError_t e2 = cudaFreeAsync(ab, s);
   return e != cudaSuccess ? e : e2;
 }

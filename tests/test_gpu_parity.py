@@ -290,8 +290,8 @@ def test_hoisted_f3_bitwise_equal(chf, n, m):
         _check(b, ref, sabs)
 
 
-@pytest.mark.parametrize("n,m", [(2, 300), (3, 100), (4, 200), (8, 150), (12, 70), (16, 700), (32, 100), (64, 40),
-                                 (128, 33)])
+@pytest.mark.parametrize("n,m", [(2, 300), (3, 100), (4, 200), (8, 150), (12, 70), (16, 700), (32, 100), (36, 40),
+                                 (64, 40), (72, 20), (128, 33)])
 def test_seedsparse_f3(chf, n, m):
     """NEXT-4 seed sparsity: skipping the products of exact-zero seed slots leaves the same
     bits as the per-evaluation path (up to the sign of zero; == treats -0 == +0) for every C,
@@ -305,13 +305,13 @@ def test_seedsparse_f3(chf, n, m):
     Cs = sorted({1, n} | ({4} if n % 4 == 0 else set()))
     for C in Cs:
         b = chf.hvp_batch_seedsparse("fletcher_powell", p, v, C, pr).cpu().numpy()
-        if n <= 64 or C == n:
+        if (n <= 64 or C == n) and chf.is_supported("fletcher_powell", n, C, "hvp"):
             a = chf.hvp_batch("fletcher_powell", p, v, C, pr).cpu().numpy()
             assert np.array_equal(a, b), f"C={C}: max |diff| {np.abs(a - b).max():.3e}"
         _check(b[:ms], ref, sabs)
 
 
-@pytest.mark.parametrize("n,m", [(2, 100), (8, 70), (32, 50), (64, 9)])
+@pytest.mark.parametrize("n,m", [(2, 100), (8, 70), (32, 50), (64, 9), (128, 5)])
 def test_seedsparse_f3_hessian(chf, n, m):
     """Seed-sparse Hessian (Alg 5 output): same bits as hessian_batch up to the sign of zero,
     oracle parity."""
