@@ -301,7 +301,8 @@ def main():
     from paper_2410_22575_b200.build import source_hash
     src_hash = source_hash()
     sweep = []
-    algo_fn = {"hvp": chf.hvp_batch, "sym_hvp": chf.sym_hvp_batch, "hvp_hoisted": chf.hvp_batch_hoisted}
+    algo_fn = {"hvp": chf.hvp_batch, "sym_hvp": chf.sym_hvp_batch, "hvp_hoisted": chf.hvp_batch_hoisted,
+               "hvp_seedsparse": chf.hvp_batch_seedsparse}
     if not args.no_sweep:
         for algo, fnb in algo_fn.items():
             for f in FUNCS:

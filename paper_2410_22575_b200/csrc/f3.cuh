@@ -81,6 +81,10 @@ CHF_INL void f3_fma(const double2& c, int kk, const V& v, double (&Ep)[KB], doub
 #define CHF_F3_JUNROLL 1
 #endif
 constexpr int kF3JUnroll = CHF_F3_JUNROLL;  // j-loop unroll of the shared-memory (A,B) path
+#ifndef CHF_F3_RING_JUNROLL
+#define CHF_F3_RING_JUNROLL 1
+#endif
+constexpr int kF3RingJUnroll = CHF_F3_RING_JUNROLL;  // j-loop unroll of the ring path (n > 32)
 
 struct SlotVals {
   double sp, cp, sq, cq;
@@ -116,7 +120,7 @@ CHF_INL void f3_sum_j(const ABRing<KB, JC>& ab, int n, int kb, const Vals& vals,
 #pragma unroll
       for (int kk = 0; kk < KB; kk++) f3_fma<KB, true>(st[kk], kk, v, Ep, Eq);
     }
-#pragma unroll 1
+#pragma unroll kF3RingJUnroll
     for (int jj = (jc == 0 ? 1 : 0); jj < JC; jj++) {
       const SlotVals v = vals(jc * JC + jj);
 #pragma unroll
