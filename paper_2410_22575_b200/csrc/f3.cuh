@@ -82,7 +82,7 @@ CHF_INL void f3_fma(const double2& c, int kk, const V& v, double (&Ep)[KB], doub
 #endif
 constexpr int kF3JUnroll = CHF_F3_JUNROLL;  // j-loop unroll of the shared-memory (A,B) path
 #ifndef CHF_F3_RING_JUNROLL
-#define CHF_F3_RING_JUNROLL 1
+#define CHF_F3_RING_JUNROLL 2  // measured 2-5% faster than 1 at n = 64 / 128 (profiles/r01/f3ab/)
 #endif
 constexpr int kF3RingJUnroll = CHF_F3_RING_JUNROLL;  // j-loop unroll of the ring path (n > 32)
 
