@@ -7,7 +7,7 @@
 
 namespace chessfad {
 
-constexpr int kWarpsReg = 4;  // register path: 128 threads per CTA (2 CTAs/SM at 252 regs)
+constexpr int kWarpsReg = 4;  // register path: 128 threads per CTA (2 CTAs/SM at <= 255 regs)
 
 // groups of 32 points per CTA so that every warp of the CTA has a row to work on; the
 // symmetric HVP gives every warp its own group (it walks all rows of its points)

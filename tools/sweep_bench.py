@@ -19,6 +19,7 @@ import torch  # noqa: E402
 
 import paper_2410_22575_b200 as chf  # noqa: E402
 import synth  # noqa: E402
+from bench import executed_entry  # noqa: E402
 from paper_2410_22575_b200.build import source_hash  # noqa: E402
 
 PEAK = 148 * 64 * 2 * 1.965e9 / 1e12
@@ -37,11 +38,6 @@ def main():
     dev = torch.device("cuda", 0)
     n = args.n
     Cs = args.csizes or [c for c in (1, 2, 4, 8, 16, 32, 64, 128) if c <= n and n % c == 0]
-    try:
-        tab = json.load(open(os.path.join(ROOT, "profiles", "executed_flops.json")))
-        tab = tab["entries"] if tab.get("src_hash") == source_hash() else {}
-    except Exception:
-        tab = {}
     hess = args.algo in ("hessian", "sym_hessian", "hessian_seedsparse")
     fn = {"hvp": chf.hvp_batch, "sym_hvp": chf.sym_hvp_batch, "hessian": chf.hessian_batch, "hvp_hoisted": chf.hvp_batch_hoisted, "hvp_seedsparse": chf.hvp_batch_seedsparse, "hessian_seedsparse": chf.hessian_batch_seedsparse,
           "sym_hessian": chf.sym_hessian_batch}[args.algo]
@@ -70,8 +66,9 @@ def main():
             torch.cuda.synchronize()
             t = e0.elapsed_time(e1) / 1e3 / reps
             mf = chf.model_flops_per_point(f, n, c, algo=args.algo)
-            key = f"{f} n={n} C={c}" + ("" if args.algo == "hvp" else f" {args.algo}")
-            ex = tab.get(key)
+            ex = executed_entry(f, n, c, source_hash(), args.algo)  # valid by kernel SASS hash (bench.py)
+            if ex is not None and ex["basis"].startswith("STALE"):
+                ex = None
             rec = {"func": f, "n": n, "C": c, "algo": args.algo, "m": m, "ms": t * 1e3, "points_per_s": m / t,
                    "model_flops_per_point": mf, "model_tflops_effective": m * mf / t / 1e12,
                    "executed_tflops": None if ex is None else m * ex["executed_flops_per_point"] / t / 1e12}
