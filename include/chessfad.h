@@ -120,17 +120,19 @@ int chessfad_hvp_batch_hoisted(int func, int n, int csize, int64_t m, const doub
                                double *out, const double *params, void *stream);
 
 /*
- * NEXT-4 seed sparsity (beyond the paper), Fletcher-Powell only: Alg 7 with the
- * terms that multiply an exact zero seed slot skipped.  A CHUNK-INIT seed (Alg 4,
- * PAPER.md:172-194) has derivative 1 in slot 1 only for variable i and in slot 2+c only for
- * variable cs+c, so each derivative slot of the E_k sums of F3 has ONE nonzero term; the
- * value slot does not depend on the seed and is formed once per point.  Work per point
- * O(n^3) instead of O(n^4/C); every remaining operation is the one the per-evaluation path
- * performs, in the same order, so with finite inputs `out` equals chessfad_hvp_batch's bit for
- * bit up to the sign of zero, for every C (C only has to be a valid chunk size).  Executed FLOPs
+ * NEXT-4 seed sparsity (beyond the paper): Alg 7 with the operations on exact-zero
+ * seed slots skipped.  Rosenbrock, Ackley, prodsum: only the terms of the running sums that
+ * touch variable i or the chunk are evaluated as hDuals (the others have derivative slots
+ * that are exact +-0), O(C) instead of O(n) hDual ops per evaluation.  Fletcher-Powell: a
+ * CHUNK-INIT seed (Alg 4) has derivative 1 in slot 1 only for variable i and
+ * in slot 2+c only for variable cs+c, so each derivative slot of the E_k sums of F3 has ONE
+ * nonzero term; the value slot does not depend on the seed and is formed once per point; work
+ * per point O(n^3) instead of O(n^4/C), the same for every C.  Every remaining operation is
+ * the one the per-evaluation path performs, in the same order, so with finite inputs `out`
+ * equals chessfad_hvp_batch's bit for bit up to the sign of zero.  Executed FLOPs
  * are far BELOW the model count (CHESSFAD_ALGO_HVP_SEEDSPARSE reports the paper's model);
  * rates against the model are "effective".  Arguments and errors as chessfad_hvp_batch;
- * ERR_UNSUPPORTED for the other functions and for n > 128.
+ * ERR_UNSUPPORTED outside the per-evaluation kernels' shapes (Fletcher-Powell: n > 128).
  */
 int chessfad_hvp_batch_seedsparse(int func, int n, int csize, int64_t m, const double *points, const double *vecs,
                                   double *out, const double *params, void *stream);
@@ -138,7 +140,7 @@ int chessfad_hvp_batch_seedsparse(int func, int n, int csize, int64_t m, const d
 /*
  * The same seed sparsity for the Hessian API (Alg 5 output): hess[e*n*n + i*n + j] as
  * chessfad_hessian_batch, bit-identical to it up to the sign of zero.  Arguments and errors
- * as chessfad_hessian_batch; Fletcher-Powell only, n <= 128.
+ * as chessfad_hessian_batch (Fletcher-Powell: n <= 128).
  */
 int chessfad_hessian_batch_seedsparse(int func, int n, int csize, int64_t m, const double *points, double *hess,
                                       const double *params, void *stream);

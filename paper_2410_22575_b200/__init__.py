@@ -148,8 +148,8 @@ def hvp_batch_hoisted(func, points, vecs, csize: int, params=None, out=None, str
 
 
 def hvp_batch_seedsparse(func, points, vecs, csize: int, params=None, out=None, stream=None):
-    """NEXT-4 seed sparsity (Fletcher-Powell): Alg 7 with the products of exact-zero seed slots
-    skipped, O(n^3) per point; equals hvp_batch bit for bit up to the sign of zero."""
+    """NEXT-4 seed sparsity (every function): Alg 7 with the operations on exact-zero seed slots
+    skipped; equals hvp_batch bit for bit up to the sign of zero."""
     return _hvp("chessfad_hvp_batch_seedsparse", func, points, vecs, csize, params, out, stream)
 
 
@@ -198,8 +198,8 @@ def hessian_grad_batch(func, points, csize: int, params=None, out=None, grad=Non
 
 
 def hessian_batch_seedsparse(func, points, csize: int, params=None, out=None, stream=None):
-    """NEXT-4 seed sparsity for the Hessian API (Fletcher-Powell): equals hessian_batch bit for
-    bit up to the sign of zero, O(n^3) per point."""
+    """NEXT-4 seed sparsity for the Hessian API (every function): equals hessian_batch bit for
+    bit up to the sign of zero."""
     return _hess("chessfad_hessian_batch_seedsparse", func, points, csize, params, out, stream)
 
 

@@ -69,8 +69,31 @@ int supported(int func, int n, int csize, int mode) {
 // seed-sparse HVP (NEXT-4): Fletcher-Powell only; every C | n gives the same result (the
 // columns of all chunks are formed one by one), so csize only has to be valid
 bool sparse_supported(int func, int n) {
-  return func == CHESSFAD_FLETCHER_POWELL && n <= kMaxNF3 &&
-         f3_sparse_smem_bytes(n, groups_for(n, kWarpsF3, MODE_HVP)) <= kSmemMax;
+  if (func != CHESSFAD_FLETCHER_POWELL)  // register path: same shapes as the per-evaluation kernels
+    return supported(func, n, 1, MODE_HVP) && supported(func, n, 1, MODE_HESS);
+  return n <= kMaxNF3 && f3_sparse_smem_bytes(n, groups_for(n, kWarpsF3, MODE_HVP)) <= kSmemMax;
+}
+
+// register path: the chunk runs as column groups of the largest compiled c' (reg_kernel_chunk)
+template <int MODE>
+cudaError_t dispatch_sparse_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s) {
+  const int C = reg_kernel_chunk(Capi);
+#define CHF_SPR_CASE(F)                                           \
+  switch (C) {                                                    \
+    case 1: return launch_sparse_reg<F, 1, MODE>(a, s);           \
+    case 2: return launch_sparse_reg<F, 2, MODE>(a, s);           \
+    case 4: return launch_sparse_reg<F, 4, MODE>(a, s);           \
+    case 8: return launch_sparse_reg<F, 8, MODE>(a, s);           \
+    case 16: return launch_sparse_reg<F, 16, MODE>(a, s);         \
+  }                                                               \
+  break;
+  switch (func) {
+    case CHESSFAD_ROSENBROCK: CHF_SPR_CASE(FUNC_ROSENBROCK)
+    case CHESSFAD_ACKLEY: CHF_SPR_CASE(FUNC_ACKLEY)
+    case CHESSFAD_PRODSUM: CHF_SPR_CASE(FUNC_PRODSUM)
+  }
+#undef CHF_SPR_CASE
+  return cudaErrorInvalidValue;
 }
 
 #ifndef CHF_SP_CB
@@ -93,6 +116,10 @@ int sparse_entry(int func, int n, int csize, int64_t m, const double* points, co
   a.vecs = vecs;
   a.out = out;
   a.params = params;
+  if (func != CHESSFAD_FLETCHER_POWELL) {
+    const cudaError_t er = dispatch_sparse_reg<HESS ? MODE_HESS : MODE_HVP>(func, csize, a, (cudaStream_t)stream);
+    return er == cudaSuccess ? CHESSFAD_OK : CHESSFAD_ERR_CUDA;
+  }
   cudaError_t e = cudaErrorInvalidValue;
   int cb = CHF_SP_CB;  // column block: largest power of two <= CHF_SP_CB dividing n
   while (n % cb) cb >>= 1;

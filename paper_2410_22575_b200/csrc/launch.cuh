@@ -148,6 +148,17 @@ CHF_FOR_C(CHF_DECL_REG, FUNC_ROSENBROCK)
 CHF_FOR_C(CHF_DECL_REG, FUNC_ACKLEY)
 CHF_FOR_C(CHF_DECL_REG, FUNC_PRODSUM)
 
+// NEXT-4 seed sparsity for F1/F2/F4 (testfuncs.cuh SparseFunc), HVP and Hessian
+template <int FUNC, int C, int MODE>
+cudaError_t launch_sparse_reg(BatchArgs a, cudaStream_t s) {
+  return launch_functor<SparseFunc<FUNC>, C, MODE>(SparseFunc<FUNC>{}, a, s);
+}
+#define CHF_DECL_SPR1(F, C) extern template cudaError_t launch_sparse_reg<F, C, MODE_HVP>(BatchArgs, cudaStream_t); \
+  extern template cudaError_t launch_sparse_reg<F, C, MODE_HESS>(BatchArgs, cudaStream_t);
+CHF_FOR_C(CHF_DECL_SPR1, FUNC_ROSENBROCK)
+CHF_FOR_C(CHF_DECL_SPR1, FUNC_ACKLEY)
+CHF_FOR_C(CHF_DECL_SPR1, FUNC_PRODSUM)
+
 #define CHF_DECL_F31(KB, AB, M) extern template cudaError_t launch_f3<KB, M, AB>(BatchArgs, cudaStream_t);
 #define CHF_DECL_F3(KB) CHF_FOR_MODE(CHF_DECL_F31, KB, false) CHF_FOR_MODE(CHF_DECL_F31, KB, true) \
   CHF_DECL_F31(KB, false, MODE_HVP_ROWHOIST) CHF_DECL_F31(KB, true, MODE_HVP_ROWHOIST)

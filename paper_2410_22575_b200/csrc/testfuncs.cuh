@@ -200,6 +200,101 @@ struct BuiltinFunc {
   }
 };
 
+// ---------------------------------------------------------------- NEXT-4 seed sparsity (F1, F2, F4)
+// chessfad_hvp_batch_seedsparse / chessfad_hessian_batch_seedsparse for the register functions.
+// A CHUNK-INIT seed y(k) has nonzero derivative slots only for k in {i} U [cs, cs+C) (Alg 4,
+// PAPER.md:172-194).  A term of a running sum whose operands are all constant seeds has
+// derivative slots that are exact +-0, so it changes no derivative slot of the sum (up to the
+// sign of zero); only the ACTIVE terms -- those touching {i} U [cs, cs+C) -- are evaluated as
+// hDuals, in the same ascending order and with the same operations as f_rosenbrock /
+// f_ackley / f_prodsum.  The value slot of a sum is needed only where a later unary rule reads
+// it (Ackley's s1, s2); it is formed over all terms in the same chain as the full evaluation.
+// Work per evaluation: O(C) hDual ops instead of O(n).  Executed FLOPs are far below the model.
+
+// ascending k in [lo1, hi1] U [lo2, hi2] (each clipped to [0, kmax]), each k once
+template <class Body>
+CHF_INL void sp_union(int lo1, int hi1, int lo2, int hi2, int kmax, Body&& body) {
+  lo1 = max(lo1, 0); hi1 = min(hi1, kmax);
+  lo2 = max(lo2, 0); hi2 = min(hi2, kmax);
+  if (lo2 < lo1) {  // order the intervals
+    int t = lo1; lo1 = lo2; lo2 = t;
+    t = hi1; hi1 = hi2; hi2 = t;
+  }
+  if (lo1 <= hi1) {
+    for (int k = lo1; k <= hi1; k++) body(k);
+    lo2 = max(lo2, hi1 + 1);
+  }
+  for (int k = lo2; k <= hi2; k++) body(k);
+}
+
+template <int C>
+CHF_INL hd<C> hd_zero() {
+  hd<C> r;
+#pragma unroll
+  for (int s = 0; s < hd<C>::N; s++) r.v[s] = 0.0;
+  return r;
+}
+
+// F1: terms k touch y_k, y_{k+1}: active k in {i-1, i} U [cs-1, cs+C-1]; the value slot of s is dead
+template <int C>
+CHF_INL hd<C> fsp_rosenbrock(int n, const LaneSeed<C>& y) {
+  hd<C> s = hd_zero<C>();
+  sp_union(y.i - 1, y.i, y.cs - 1, y.cs + C - 1, n - 2, [&](int k) {
+    const hd<C> yk = y(k), yk1 = y(k + 1);
+    const hd<C> d = hd_fnma(yk, yk, yk1);
+    const hd<C> e = 1.0 - yk;
+    s = hd_fma(e, e, hd_axpy(100.0, d * d, s));
+  });
+  return s;
+}
+
+// F4: as F1
+template <int C>
+CHF_INL hd<C> fsp_prodsum(int n, const LaneSeed<C>& y) {
+  hd<C> s = hd_zero<C>();
+  sp_union(y.i - 1, y.i, y.cs - 1, y.cs + C - 1, n - 2, [&](int k) { s = hd_fma(y(k), y(k + 1), s); });
+  return s;
+}
+
+// F2: s1 = sum y_k^2, s2 = sum cos(2 pi y_k): active k in {i} U [cs, cs+C); value slots over all k
+template <int C>
+CHF_INL hd<C> fsp_ackley(int n, const LaneSeed<C>& y) {
+  const double two_pi = 6.283185307179586, euler = 2.718281828459045;
+  hd<C> s1 = hd_zero<C>(), s2 = hd_zero<C>();
+  sp_union(y.i, y.i, y.cs, y.cs + C - 1, n - 1, [&](int k) {
+    const hd<C> yk = y(k);
+    s1 = hd_fma(yk, yk, s1);
+    const hd<C> u = two_pi * yk;
+    s2 = hd_unary_acc(u, y.cos2pi[k * y.stride], -y.sin2pi[k * y.stride], -y.cos2pi[k * y.stride], s2);
+  });
+  {  // value slots: the chains of f_ackley (first term initialises)
+    const double a0 = y.a[0];
+    double v1 = a0 * a0, v2 = y.cos2pi[0];
+    for (int k = 1; k < n; k++) {
+      const double ak = y.a[k * y.stride];
+      v1 = __fma_rn(ak, ak, v1);
+      v2 = v2 + y.cos2pi[k * y.stride];
+    }
+    s1.v[0] = v1;
+    s2.v[0] = v2;
+  }
+  const double inv_n = 1.0 / n;
+  const hd<C> t1 = (-20.0) * exp((-0.2) * sqrt(s1 * inv_n));
+  const hd<C> t2 = exp(s2 * inv_n);
+  return (t1 - t2) + (20.0 + euler);
+}
+
+template <int FUNC>
+struct SparseFunc {
+  static constexpr bool kTrig2Pi = FUNC == FUNC_ACKLEY;
+  template <int C, class Seed>
+  CHF_INL hd<C> operator()(int n, const Seed& y) const {
+    if constexpr (FUNC == FUNC_ROSENBROCK) return fsp_rosenbrock<C>(n, y);
+    else if constexpr (FUNC == FUNC_ACKLEY) return fsp_ackley<C>(n, y);
+    else return fsp_prodsum<C>(n, y);
+  }
+};
+
 template <class F, class = void>
 struct uses_trig2pi {
   static constexpr bool value = false;

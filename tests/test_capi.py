@@ -162,25 +162,25 @@ def test_hoisted_contract():
 
 
 def test_seedsparse_contract(lib):
-    """NEXT-4 seed sparsity: Fletcher-Powell only, any valid C, n <= 128; errors before CUDA."""
+    """NEXT-4 seed sparsity: every function (F3: n <= 128), any valid C; errors before CUDA."""
     import paper_2410_22575_b200 as chf
     for n, C in ((2, 1), (16, 4), (16, 16), (64, 8), (128, 128), (12, 3)):
         assert chf.is_supported("fletcher_powell", n, C, "hvp_seedsparse")
     assert not chf.is_supported("fletcher_powell", 256, 16, "hvp_seedsparse")
     for f in ("rosenbrock", "ackley", "prodsum"):
-        assert not chf.is_supported(f, 16, 4, "hvp_seedsparse")
+        assert chf.is_supported(f, 16, 4, "hvp_seedsparse")
+        assert chf.is_supported(f, 128, 32, "hessian_seedsparse")
     assert chf.model_flops_per_point("fletcher_powell", 16, 4, algo="hvp_seedsparse") == \
         chf.model_flops_per_point("fletcher_powell", 16, 4)
     vp = ctypes.c_void_p
     f = lib.chessfad_hvp_batch_seedsparse
-    assert f(0, 16, 4, 10, vp(1), vp(1), vp(1), None, None) == 4  # Rosenbrock: ERR_UNSUPPORTED
+    assert f(0, 1, 1, 10, vp(1), vp(1), vp(1), None, None) == 3  # Rosenbrock n = 1: ERR_FUNC
     assert f(2, 16, 4, 10, vp(1), vp(1), vp(1), None, None) == 3  # F3 without params: ERR_FUNC
     assert f(2, 16, 3, 10, vp(1), vp(1), vp(1), vp(1), None) == 2  # 3 does not divide 16: ERR_CHUNK
     assert f(2, 16, 4, 0, None, None, None, vp(1), None) == 0     # m = 0: no-op
     h = lib.chessfad_hessian_batch_seedsparse
     assert chf.is_supported("fletcher_powell", 32, 4, "hessian_seedsparse")
-    assert not chf.is_supported("ackley", 32, 4, "hessian_seedsparse")
-    assert h(1, 16, 4, 10, vp(1), vp(1), None, None) == 4  # Ackley: ERR_UNSUPPORTED
+    assert h(9, 16, 4, 10, vp(1), vp(1), None, None) == 3  # unknown function: ERR_FUNC
     assert h(2, 16, 4, 10, vp(1), None, vp(1), None) == 1  # NULL hess: ERR_ARG
     assert chf.model_flops_per_point("fletcher_powell", 32, 4, algo="hessian_seedsparse") == \
         chf.model_flops_per_point("fletcher_powell", 32, 4, hessian=True)

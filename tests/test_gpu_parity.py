@@ -329,6 +329,35 @@ def test_seedsparse_f3_hessian(chf, n, m):
 
 
 @pytest.mark.parametrize("func", ["rosenbrock", "ackley", "prodsum"])
+@pytest.mark.parametrize("n,m", [(2, 100), (3, 70), (8, 100), (16, 300), (24, 60), (64, 40), (128, 20)])
+def test_seedsparse_register_functions(chf, func, n, m):
+    """NEXT-4 seed sparsity, F1/F2/F4: only the terms touching {i} U chunk are evaluated as
+    hDuals; same bits as the per-evaluation path up to the sign of zero (HVP and Hessian, every
+    compiled C and a column-group C), oracle parity, bit-exact integer pins."""
+    P, V = synth.points(29, n, m), synth.vectors(29, n, m)
+    dev = torch.device("cuda")
+    p, v = torch.from_numpy(P).to(dev), torch.from_numpy(V).to(dev)
+    ref, sabs = oracle.hvp_batch(func, P, V, 1)
+    for C in sorted({1, n if n <= 32 else 32} | ({2} if n % 2 == 0 else set())):
+        a = chf.hvp_batch(func, p, v, C).cpu().numpy()
+        b = chf.hvp_batch_seedsparse(func, p, v, C).cpu().numpy()
+        assert np.array_equal(a, b), f"C={C}: max |diff| {np.abs(a - b).max():.3e}"
+        _check(b, ref, sabs)
+        if n <= 64:
+            Ha = chf.hessian_batch(func, p[:16], C).cpu().numpy()
+            Hb = chf.hessian_batch_seedsparse(func, p[:16], C).cpu().numpy()
+            assert np.array_equal(Ha, Hb)
+    if func != "ackley":
+        Pi, Vi = synth.int_points(31, n, 50), synth.int_vectors(31, n, 50)
+        want = np.zeros((50, n))
+        for e in range(50):
+            H = cf.rosenbrock_hessian_exact(Pi[e]) if func == "rosenbrock" else cf.prodsum_hessian_exact(n)
+            want[e] = [float(x) for x in cf.exact_hvp(H, Vi[e])]
+        got = chf.hvp_batch_seedsparse(func, torch.from_numpy(Pi).cuda(), torch.from_numpy(Vi).cuda(), 1).cpu().numpy()
+        assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("func", ["rosenbrock", "ackley", "prodsum"])
 @pytest.mark.parametrize("n", [2, 4, 8, 12, 16])
 def test_hoisted_register_functions(chf, func, n):
     """Compile-time kernels (n in {2,4,8,16}; n = 12 falls back to the per-evaluation path):
