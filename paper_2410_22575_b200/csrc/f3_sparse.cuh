@@ -85,8 +85,32 @@ struct SpRing {
   double2* col;  // [2][kSpKS], this warp's
 };
 
+// one stage (kSpKS k-values) of a staged block, no barriers inside
 template <int CB, bool ROW0, bool COL0>
-CHF_INL void f3_sp_block_staged(int n, int i, int cb, double si, double ci, const double2* __restrict__ ab,
+CHF_INL void f3_sp_stage(int k0, double si, double ci, const double2* __restrict__ blk, const double2* __restrict__ col,
+                         const double (&sc)[CB], const double (&cc)[CB], double (&fC)[CB]) {
+#pragma unroll
+  for (int kk = 0; kk < kSpKS; kk++) {
+    const int k = k0 + kk;
+    const double2 c1 = col[kk];
+    const double r1 = -f3_sp_term<ROW0>(c1.x, ci, c1.y, -si);
+#pragma unroll
+    for (int q = 0; q < CB; q++) {
+      const double2 c = blk[kk * CB + q];
+      const double r2 = (COL0 && q == 0) ? -f3_sp_term<true>(c.x, cc[q], c.y, -sc[q])
+                                         : -f3_sp_term<false>(c.x, cc[q], c.y, -sc[q]);
+      const double t = __dmul_rn(r1, r2);
+      const double rr = __fma_rn(r1, r2, t);
+      fC[q] = (k == 0) ? rr : __dadd_rn(fC[q], rr);
+    }
+  }
+}
+
+// The barriers of the staged pipeline must be the SAME instructions in every warp (warps with
+// row 0 / column block 0 take other term forms), so row0 / col0 are runtime (warp-uniform)
+// flags here and only the barrier-free stage compute is specialised.
+template <int CB>
+CHF_INL void f3_sp_block_staged(int n, int i, int cb, bool row0, double si, double ci, const double2* __restrict__ ab,
                                 const SpRing& rg, const double* __restrict__ sa, const double* __restrict__ ca,
                                 double (&fC)[CB]) {
   double sc[CB], cc[CB];
@@ -95,6 +119,7 @@ CHF_INL void f3_sp_block_staged(int n, int i, int cb, double si, double ci, cons
     sc[q] = sa[(cb + q) * kPad];
     cc[q] = ca[(cb + q) * kPad];
   }
+  const bool col0 = cb == 0;
   const int S = n / kSpKS, lane = threadIdx.x & 31;
   auto issue = [&](int st) {
     const int k0 = st * kSpKS, buf = st & 1;
@@ -113,31 +138,22 @@ CHF_INL void f3_sp_block_staged(int n, int i, int cb, double si, double ci, cons
     if (st + 1 < S) issue(st + 1);
     const double2* blk = rg.blk + (st & 1) * kSpKS * CB;
     const double2* col = rg.col + (st & 1) * kSpKS;
-#pragma unroll
-    for (int kk = 0; kk < kSpKS; kk++) {
-      const int k = st * kSpKS + kk;
-      const double2 c1 = col[kk];
-      const double r1 = -f3_sp_term<ROW0>(c1.x, ci, c1.y, -si);
-#pragma unroll
-      for (int q = 0; q < CB; q++) {
-        const double2 c = blk[kk * CB + q];
-        const double r2 = (COL0 && q == 0) ? -f3_sp_term<true>(c.x, cc[q], c.y, -sc[q])
-                                           : -f3_sp_term<false>(c.x, cc[q], c.y, -sc[q]);
-        const double t = __dmul_rn(r1, r2);
-        const double rr = __fma_rn(r1, r2, t);
-        fC[q] = (k == 0) ? rr : __dadd_rn(fC[q], rr);
-      }
+    const int k0 = st * kSpKS;
+    if (row0) {
+      if (col0) f3_sp_stage<CB, true, true>(k0, si, ci, blk, col, sc, cc, fC);
+      else f3_sp_stage<CB, true, false>(k0, si, ci, blk, col, sc, cc, fC);
+    } else {
+      if (col0) f3_sp_stage<CB, false, true>(k0, si, ci, blk, col, sc, cc, fC);
+      else f3_sp_stage<CB, false, false>(k0, si, ci, blk, col, sc, cc, fC);
     }
   }
 }
 
 // row i: out_i = sum_col d2f/dx_i dx_col * v_col, ascending columns (HVP), or the row stored
 // to hrow (HESS; nullptr for ragged-tail lanes)
-template <int CB, bool ROW0, bool HESS, bool STAGED>
-CHF_INL double f3_sp_row(int n, int i, const double2* __restrict__ ab, const double* __restrict__ sa,
-                         const double* __restrict__ ca, const double* __restrict__ r0t, const double* __restrict__ v,
-                         int vs, double* __restrict__ hrow, const SpRing& rg) {
-  const double si = sa[i * kPad], ci = ca[i * kPad];
+template <bool ROW0>
+CHF_INL double f3_sp_diag(int n, int i, double si, double ci, const double2* __restrict__ ab,
+                          const double* __restrict__ r0t) {
   // diagonal column: the full slot set (r0, r1 = r2, rC), f3_phase_b's expression
   double fdiag = 0.0;
   for (int k = 0; k < n; k++) {
@@ -151,15 +167,27 @@ CHF_INL double f3_sp_row(int n, int i, const double2* __restrict__ ab, const dou
     const double rrC = r0 * rC + r1 * r2 + r1 * r2 + r0 * rC;
     fdiag = (k == 0) ? rrC : fdiag + rrC;
   }
+  return fdiag;
+}
+
+// row0 is a runtime flag so that the staged path's barriers are shared by all warps
+template <int CB, bool HESS, bool STAGED>
+CHF_INL double f3_sp_row(int n, int i, bool row0, const double2* __restrict__ ab, const double* __restrict__ sa,
+                         const double* __restrict__ ca, const double* __restrict__ r0t, const double* __restrict__ v,
+                         int vs, double* __restrict__ hrow, const SpRing& rg) {
+  const double si = sa[i * kPad], ci = ca[i * kPad];
+  const double fdiag = row0 ? f3_sp_diag<true>(n, i, si, ci, ab, r0t) : f3_sp_diag<false>(n, i, si, ci, ab, r0t);
   double res = 0.0;
   for (int cb = 0; cb < n; cb += CB) {
     double fC[CB];
     if constexpr (STAGED) {
-      if (cb == 0) f3_sp_block_staged<CB, ROW0, true>(n, i, cb, si, ci, ab, rg, sa, ca, fC);
-      else f3_sp_block_staged<CB, ROW0, false>(n, i, cb, si, ci, ab, rg, sa, ca, fC);
+      f3_sp_block_staged<CB>(n, i, cb, row0, si, ci, ab, rg, sa, ca, fC);
+    } else if (row0) {
+      if (cb == 0) f3_sp_block<CB, true, true>(n, i, cb, si, ci, ab, sa, ca, fC);
+      else f3_sp_block<CB, true, false>(n, i, cb, si, ci, ab, sa, ca, fC);
     } else {
-      if (cb == 0) f3_sp_block<CB, ROW0, true>(n, i, cb, si, ci, ab, sa, ca, fC);
-      else f3_sp_block<CB, ROW0, false>(n, i, cb, si, ci, ab, sa, ca, fC);
+      if (cb == 0) f3_sp_block<CB, false, true>(n, i, cb, si, ci, ab, sa, ca, fC);
+      else f3_sp_block<CB, false, false>(n, i, cb, si, ci, ab, sa, ca, fC);
     }
 #pragma unroll
     for (int q = 0; q < CB; q++) {
@@ -236,8 +264,7 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, CHF_SP_MINB) hvp_f3_sparse_kern
   const SpRing rg{s_ab, s_ab + 2 * kSpKS * CB + warp * 2 * kSpKS};
   for (int i = wg; i < n; i += rstep) {
     double* hrow = (HESS && e < p.m) ? p.out + (e * n + i) * n : nullptr;
-    const double res = (i == 0) ? f3_sp_row<CB, true, HESS, STAGED>(n, i, ab, sa, ca, r0t, v, vs, hrow, rg)
-                                : f3_sp_row<CB, false, HESS, STAGED>(n, i, ab, sa, ca, r0t, v, vs, hrow, rg);
+    const double res = f3_sp_row<CB, HESS, STAGED>(n, i, i == 0, ab, sa, ca, r0t, v, vs, hrow, rg);
     if (HESS) {
     } else if (SLIM) {
       if (e < p.m) p.out[e * n + i] = res;
