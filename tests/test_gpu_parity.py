@@ -388,8 +388,9 @@ def _sampled_check(chf, func, n, m, C, algo="hvp", nsample=24, seed=0):
     p, v = torch.from_numpy(P).to(dev), torch.from_numpy(V).to(dev)
     pr = None if params is None else torch.from_numpy(params).to(dev)
     idx = np.unique(np.concatenate([[0, m - 1], np.linspace(0, m - 1, nsample).astype(np.int64)]))
-    if algo in ("hessian", "sym_hessian"):
-        fn = chf.hessian_batch if algo == "hessian" else chf.sym_hessian_batch
+    if algo in ("hessian", "sym_hessian", "hessian_seedsparse"):
+        fn = {"hessian": chf.hessian_batch, "sym_hessian": chf.sym_hessian_batch,
+              "hessian_seedsparse": chf.hessian_batch_seedsparse}[algo]
         H = fn(func, p, C, pr)
         got = H[torch.from_numpy(idx).to(dev)].cpu().numpy()
         del H
@@ -397,7 +398,8 @@ def _sampled_check(chf, func, n, m, C, algo="hvp", nsample=24, seed=0):
         scale = np.abs(ref).reshape(idx.size, -1).max(axis=1)
         assert (np.abs(got - ref).reshape(idx.size, -1).max(axis=1) / scale).max() <= TIGHT
     else:
-        fn = {"hvp": chf.hvp_batch, "sym_hvp": chf.sym_hvp_batch}[algo]
+        fn = {"hvp": chf.hvp_batch, "sym_hvp": chf.sym_hvp_batch, "hvp_hoisted": chf.hvp_batch_hoisted,
+              "hvp_seedsparse": chf.hvp_batch_seedsparse}[algo]
         got = fn(func, p, v, C, pr)[torch.from_numpy(idx).to(dev)].cpu().numpy()
         ref, sabs = oracle.hvp_batch(func, P[idx], V[idx], C, params)
         _check(got, ref, sabs)
@@ -429,6 +431,17 @@ def test_config5_full_size_sampled(chf):
     """cfg5: n = 16, m = 2^23 on one GPU (the strong-scaling total), C = 16."""
     _sampled_check(chf, "rosenbrock", 16, 1 << 23, 16, nsample=32)
     _sampled_check(chf, "rosenbrock", 16, 1 << 23, 4, algo="sym_hvp", nsample=32)
+
+
+@pytest.mark.parametrize("func", FUNCS)
+def test_next4_full_size_sampled(chf, func):
+    """NEXT-4 entry points at the bench's cfg2 shape (n = 16, m = 2^20, as bench.py's sweep
+    times them), the seed-sparse ones also at n = 128, m = 2^20, and the seed-sparse Hessian
+    at cfg4 (n = 32, m = 2^18)."""
+    _sampled_check(chf, func, 16, 1 << 20, 16, algo="hvp_hoisted", nsample=16)
+    _sampled_check(chf, func, 16, 1 << 20, 4, algo="hvp_seedsparse", nsample=16)
+    _sampled_check(chf, func, 128, 1 << 20, 16, algo="hvp_seedsparse", nsample=4 if func == "fletcher_powell" else 8)
+    _sampled_check(chf, func, 32, 1 << 18, 8, algo="hessian_seedsparse", nsample=8)
 
 
 # ------------------------------------------------------------ the paper's Fig. 2 L2 design (comparison baseline)
