@@ -99,6 +99,9 @@ cudaError_t dispatch_sparse_reg(int func, int Capi, const BatchArgs& a, cudaStre
 #ifndef CHF_SP_CB
 #define CHF_SP_CB 16  // column block of the seed-sparse kernel (tuning knob; power of two <= 16)
 #endif
+#ifndef CHF_SP_CB_SMEM
+#define CHF_SP_CB_SMEM 8  // ... with (A, B) in shared memory (n <= 32): 3 CTAs/SM (measured)
+#endif
 
 template <bool HESS>
 int sparse_entry(int func, int n, int csize, int64_t m, const double* points, const double* vecs, double* out,
@@ -121,7 +124,8 @@ int sparse_entry(int func, int n, int csize, int64_t m, const double* points, co
     return er == cudaSuccess ? CHESSFAD_OK : CHESSFAD_ERR_CUDA;
   }
   cudaError_t e = cudaErrorInvalidValue;
-  int cb = CHF_SP_CB;  // column block: largest power of two <= CHF_SP_CB dividing n
+  // column block: largest power of two <= CHF_SP_CB (n <= 32: <= CHF_SP_CB_SMEM) dividing n
+  int cb = n <= 32 ? CHF_SP_CB_SMEM : CHF_SP_CB;
   while (n % cb) cb >>= 1;
   switch (cb) {
 #define CHF_CASE_SP(CB) \

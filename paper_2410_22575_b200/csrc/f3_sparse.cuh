@@ -31,7 +31,10 @@
 #define CHF_SP_KUNROLL 4  // k-loop unroll of the column-block loop (measured 4 > 2: profiles/r01/sparse/)
 #endif
 #ifndef CHF_SP_MINB
-#define CHF_SP_MINB 2  // min CTAs/SM (register budget) of the seed-sparse kernel (tuning knob)
+#define CHF_SP_MINB 2  // min CTAs/SM (register budget) of the seed-sparse kernel, n > 32 (tuning knob)
+#endif
+#ifndef CHF_SP_MINB_SMEM
+#define CHF_SP_MINB_SMEM 3  // ... with (A, B) in shared memory, n <= 32 (column blocks of <= 8)
 #endif
 
 namespace chessfad {
@@ -208,7 +211,7 @@ CHF_INL double f3_sp_row(int n, int i, bool row0, const double2* __restrict__ ab
 // STAGED (SLIM, n % kSpKS == 0): the CTA-shared (A, B) block rows go through the cp.async
 // double buffer (f3_sp_block_staged); every warp then has n / 4 rows (uniform barriers).
 template <int CB, bool AB_SMEM, bool SLIM, bool HESS, bool STAGED>
-__global__ void __launch_bounds__(kWarpsF3 * 32, CHF_SP_MINB) hvp_f3_sparse_kernel(BatchArgs p, const double2* __restrict__ ab_g) {
+__global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? CHF_SP_MINB_SMEM : CHF_SP_MINB) hvp_f3_sparse_kernel(BatchArgs p, const double2* __restrict__ ab_g) {
   extern __shared__ double smem[];
   const int n = p.n, G = p.groups, P = 32 * G;
   double* s_sa = smem;                 // [G][n][33]  sin a
