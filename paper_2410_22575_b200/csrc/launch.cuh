@@ -7,7 +7,10 @@
 
 namespace chessfad {
 
-constexpr int kWarpsReg = 4;  // register path: 128 threads per CTA (2 CTAs/SM at <= 255 regs)
+#ifndef CHF_WARPS_REG
+#define CHF_WARPS_REG 4  // measured vs 2 and 8: profiles/r01/warps/ (2: neutral but Ackley n = 64 +16%; 8: up to +35%)
+#endif
+constexpr int kWarpsReg = CHF_WARPS_REG;  // register path: 128 threads per CTA (2 CTAs/SM at <= 255 regs)
 
 // groups of 32 points per CTA so that every warp of the CTA has a row to work on; the
 // symmetric HVP gives every warp its own group (it walks all rows of its points)
