@@ -8,19 +8,28 @@ A step is one chessfad_hvp_batch call: every §8(a) row (load points/vectors, se
 propagate hDual<C>, chunk dot, row sum, store) over m synthetic points on each GPU
 (weak scaling: m points per GPU, disjoint index ranges of one seeded stream).  The headline
 workload is BASELINE.json configs[1] (cfg2: n = 16, m = 2^20) with Rosenbrock, the function
-of the paper's L2 kernel; the chunk sweep over all four functions is in
-"sweep".  Timing: CUDA events on the launching stream, barrier + synchronize around the K
-timed steps, max over ranks.  Inputs (384 MiB per step) are larger than the 126 MB L2.
+of the paper's L2 kernel.  Timing: CUDA events on the launching stream, one
+per step, barrier + synchronize around the K timed steps, max over ranks; value = K-step
+mean, step_ms = median / best of the K per-step samples (§8(d)).  Inputs (384 MiB per
+step) are larger than the 126 MB L2, so no flush is needed between steps.
 
---impl reference times the CPU oracle (oracle/, plain C) on the host cores on a bounded
-sample of the same workload (the reference arm of this tier: there is no reference code).
+stdout ends with ONE compact JSON line (< 2 KB).  The bulky evidence -- the chunk sweep over
+the four functions and the algorithms, the paper's Fig. 2 kernel -- goes to --sweep-out
+(default gpurun_out/bench_sweep.json).  "strong" is BASELINE configs[4] (cfg5: 2^23 points
+split over the ranks, compute-only and compute + NCCL all-gather of the results).
+
+--gpus N without a torchrun environment re-executes itself under torch.distributed.run
+(N ranks, 127.0.0.1).  --impl reference times the CPU oracle (oracle/, plain C) on the host
+cores on a bounded sample of the same workload (the reference arm of this tier: there is
+no reference code); under N ranks only rank 0 runs it.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
@@ -37,6 +46,7 @@ METRIC = "Hessian-vector products/sec (FP64) vs n and chunk size; % of B200 FP64
 UNIT = "HVP/s"
 SMS = 148
 FP64_FMA_PER_SM_CLK = 64  # B200 FP64 (non-tensor) lanes per SM, DESIGN.md "Roofline"
+CFG5_M_TOTAL = 1 << 23    # BASELINE configs[4]: 8M points sharded over the ranks
 
 
 def env_int(name, default):
@@ -64,7 +74,7 @@ class ClockSampler:
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
-    def __init__(self, device_index, period=0.02):
+    def __init__(self, device_index, period=0.005):
         self.samples, self.reasons, self.max_mhz, self.ok = [], 0, None, False
         self.period = period
         self._stop = threading.Event()
@@ -108,6 +118,33 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+# ------------------------------------------------------------------------- torchrun re-exec
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def maybe_respawn(args, argv):
+    """--gpus N > 1 outside a torchrun environment: run this script under
+    torch.distributed.run with N ranks (one per GPU) and return its exit code; None when the
+    current process is already the right one."""
+    if "WORLD_SIZE" in os.environ:
+        ws = env_int("WORLD_SIZE", 1)
+        if ws != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
+        return None
+    if args.gpus <= 1:
+        return None
+    # the arguments travel in the environment: torchrun's own parser rejects script options
+    # that abbreviate one of its options (e.g. --n)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)]
+    return subprocess.call(cmd, env=dict(os.environ, CHESSFAD_BENCH_ARGV=json.dumps(list(argv))))
+
+
 # ------------------------------------------------------------------------- oracle timing
 def oracle_rate(func, n, C, params, first, target_s, threads):
     """Time the plain CPU oracle (Alg 7, oracle/) on a bounded sample: returns HVP/s, the
@@ -125,15 +162,15 @@ def oracle_rate(func, n, C, params, first, target_s, threads):
 
 
 def run_reference(args, rank, world):
-    """Reference arm: the CPU oracle as it stands, on the host cores."""
+    """Reference arm: the CPU oracle as it stands, on the host cores (rank 0 only)."""
     if rank != 0:
         return 0
     import oracle
     oracle.build()
     threads = oracle.default_threads()
     params = synth.fp_params_flat(0, args.n) if args.func == "fletcher_powell" else None
-    # size one step to ~1.5 s so that W+K steps end within a few minutes
-    rate, m_step, _ = oracle_rate(args.func, args.n, args.csize, params, 0, 1.5, threads)
+    # one step = a bounded sample of the workload sized so that W+K steps end within minutes
+    rate, m_step, _ = oracle_rate(args.func, args.n, args.csize, params, 0, args.ref_step_s, threads)
     P, V = synth.points(0, args.n, m_step), synth.vectors(0, args.n, m_step)
     for _ in range(args.warmup):
         oracle.hvp_batch(args.func, P, V, args.csize, params, threads=threads)
@@ -158,19 +195,18 @@ def run_reference(args, rank, world):
 
 def workload_config(args, world):
     if getattr(args, "m_total", 0):
-        wl = f"cfg5: {args.func} n={args.n} C={args.csize} m={args.m_total} points over {world} GPU(s) (strong scaling)"
+        wl = f"cfg5: {args.func} n={args.n} C={args.csize} m={args.m_total} over {world} GPU(s) (strong)"
         gp = args.m_total
     else:
-        wl = f"cfg2: {args.func} n={args.n} C={args.csize} m={args.m} points per GPU (BASELINE configs[1])"
+        wl = f"cfg2: {args.func} n={args.n} C={args.csize} m={args.m} per GPU (BASELINE configs[1])"
         gp = args.m * world
-    return {"workload": wl,
-            "func": args.func, "n": args.n, "csize": args.csize, "m_per_gpu": args.m, "global_points": gp,
-            "seed": 0, "parallelism": f"dp{world} (points sharded, no collective on the data path)",
-            "l2": f"inputs larger than L2: {3 * args.m * args.n * 8 / 2**20:.0f} MiB per step vs 126 MB L2"}
+    return {"workload": wl, "func": args.func, "n": args.n, "csize": args.csize, "m_per_gpu": args.m,
+            "global_points": gp, "seed": 0, "parallelism": f"dp{world} (points sharded, no data-path collective)",
+            "l2": f"no flush: inputs {3 * args.m * args.n * 8 / 2**20:.0f} MiB per step > 126 MB L2"}
 
 
 # ------------------------------------------------------------------------- our arm
-def main():
+def parse_args(argv):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
@@ -181,14 +217,25 @@ def main():
     ap.add_argument("--csize", type=int, default=16)
     ap.add_argument("--m", type=int, default=1 << 20, help="points per GPU (weak scaling)")
     ap.add_argument("--m-total", type=int, default=0,
-                    help="strong scaling: total points split over the ranks (BASELINE cfg5: 8388608)")
-    ap.add_argument("--gather", action="store_true", help="time an all-gather of the results after the run")
+                    help="headline as strong scaling: total points split over the ranks")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-strong", action="store_true", help="skip the cfg5 strong-scaling object")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=10)
-    args = ap.parse_args()
+    ap.add_argument("--ref-step-s", type=float, default=1.5, help="reference arm: seconds of oracle work per step")
+    ap.add_argument("--sweep-out", default=os.path.join(ROOT, "gpurun_out", "bench_sweep.json"))
+    args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
+    return args
 
+
+def main(argv=None):
+    if argv is None:
+        argv = json.loads(os.environ["CHESSFAD_BENCH_ARGV"]) if "CHESSFAD_BENCH_ARGV" in os.environ else sys.argv[1:]
+    args = parse_args(argv)
+    rc = maybe_respawn(args, argv)
+    if rc is not None:
+        return rc
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
         return run_reference(args, rank, world)
@@ -201,6 +248,10 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        chf.load()  # builds if stale (file-locked); the other ranks load the result
+    if world > 1:
+        dist.barrier()
     chf.load()
     peaks = load_peaks()
     peak_tf, peak_mhz = fp64_nominal_tflops(peaks)
@@ -209,7 +260,7 @@ def main():
         if world > 1:
             dist.barrier()
 
-    from paper_2410_22575_b200.dist import gather_rows, max_over_ranks as _mor, shard
+    from paper_2410_22575_b200.dist import GatherBuffer, max_over_ranks as _mor, shard
 
     def max_over_ranks(x):
         return _mor(x, device=dev)
@@ -231,42 +282,48 @@ def main():
     params = {f: (None if v is None else torch.from_numpy(v).to(dev)) for f, v in params_np.items()}
     stream = torch.cuda.current_stream()
 
-    def timed(func, csize, steps, warmup, sampler=None):
+    def timed_steps(fn, steps, warmup, sampler=None):
+        """K launches with a CUDA event between consecutive steps: (total s, per-step s list)."""
         for _ in range(warmup):
-            chf.hvp_batch(func, pts, vec, csize, params[func], out=out)
+            fn()
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ctx = sampler if sampler is not None else _Null()
-        with ctx:
-            ev0.record(stream)
-            for _ in range(steps):
-                chf.hvp_batch(func, pts, vec, csize, params[func], out=out)
-            ev1.record(stream)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        with (sampler if sampler is not None else _Null()):
+            evs[0].record(stream)
+            for k in range(steps):
+                fn()
+                evs[k + 1].record(stream)
             torch.cuda.synchronize()
         barrier()
-        return max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
+        per = [evs[k].elapsed_time(evs[k + 1]) / 1e3 for k in range(steps)]
+        return evs[0].elapsed_time(evs[steps]) / 1e3, per
 
-    # ---- headline
+    # ---- headline: K steps of chessfad_hvp_batch (Alg 7) on the cfg2 workload
     sampler = ClockSampler(local)
-    t = timed(args.func, C, args.steps, args.warmup, sampler)
+    t_loc, per_loc = timed_steps(lambda: chf.hvp_batch(args.func, pts, vec, C, params[args.func], out=out),
+                                 args.steps, args.warmup, sampler)
+    t = max_over_ranks(t_loc)
     per_step = t / args.steps
+    step_med, step_best = max_over_ranks(float(np.median(per_loc))), max_over_ranks(min(per_loc))
     value = m_all / per_step
     flops_pt = chf.model_flops_per_point(args.func, n, C)
-    achieved_tf = m * flops_pt / per_step / 1e12  # per GPU, one launch per step
+    model_tf = m * flops_pt / per_step / 1e12  # per GPU, one launch per step
     clocks = sampler.summary()
 
-    # ---- parity of the timed output on a deterministic sample (rank 0)
+    # ---- parity of the timed output against the oracle (rank 0: every point of its shard,
+    # F3 at n > 16 on a deterministic sample)
     parity = None
     if rank == 0:
         import oracle
-        idx = np.unique(np.concatenate([[0, m - 1], np.arange(0, m, max(1, m // 61))]))
+        full = args.func != "fletcher_powell" or n <= 16
+        idx = np.arange(m) if full else np.unique(np.concatenate([[0, m - 1], np.arange(0, m, max(1, m // 509))]))
         ref, sabs = oracle.hvp_batch(args.func, P[idx], V[idx], C, params_np[args.func])
         got = out.cpu().numpy()[idx]
         err = oracle.componentwise_error(got, ref, sabs)
-        parity = {"max_componentwise_err": float(err.max()), "points_checked": int(idx.size), "bar": 1e-10,
-                  "pass": bool(err.max() <= 1e-10)}
+        parity = {"max_err": float(err.max()), "points": int(idx.size), "of": m, "bar": 1e-10,
+                  "pass": bool(err.max() <= 1e-10), "metric": "|g-r|/max(|r|, sum_j |H_ij||v_j|)"}
 
     # ---- FP64 probe (attainable DFMA rate on this GPU)
     sink = torch.empty(SMS * 8 * 256, dtype=torch.float64, device=dev)
@@ -280,81 +337,53 @@ def main():
     torch.cuda.synchronize()
     probe_tf = SMS * 8 * 256 * iters * 16 / (e0.elapsed_time(e1) / 1e3) / 1e12
 
-    # ---- e2e through the host-buffer C-ABI call (pinned host memory, copies in the timed region)
+    # ---- e2e through the host-buffer C-ABI call (pinned host memory, copies in the timed
+    # region; CUDA events on the calling stream, which the call joins before returning)
     Ph = torch.from_numpy(P).pin_memory()
     Vh = torch.from_numpy(V).pin_memory()
     Oh = torch.empty_like(Ph).pin_memory()
     ph_params = None if params_np[args.func] is None else torch.from_numpy(params_np[args.func]).pin_memory()
-    for _ in range(2):
-        chf.hvp_batch_host(args.func, Ph, Vh, C, ph_params, out=Oh)
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.e2e_steps):
-        chf.hvp_batch_host(args.func, Ph, Vh, C, ph_params, out=Oh)  # synchronous
-    e2e_t = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps)
+    host = chf.HostPipeline()
+    e2e_t, _ = timed_steps(lambda: host.hvp(args.func, Ph, Vh, C, ph_params, out=Oh), args.e2e_steps, 2)
+    e2e_t = max_over_ranks(e2e_t / args.e2e_steps)
     assert torch.equal(Oh, out.cpu()), "host-buffer path disagrees with the device path"
     e2e = {"value": m_all / e2e_t, "unit": UNIT, "h2d_bytes_per_step": 2 * m * n * 8 + (
         0 if ph_params is None else ph_params.numel() * 8), "d2h_bytes_per_step": m * n * 8,
-        "ms_per_step": e2e_t * 1e3, "api": "chessfad_hvp_batch_host (3-stage H2D/kernel/D2H stream pipeline, pinned host memory)"}
+        "ms_per_step": e2e_t * 1e3, "api": "chessfad_hvp_batch_host (pinned; H2D/kernel/D2H stream pipeline)"}
+    del host
 
-    # ---- chunk sweep over the four functions (cfg2), Alg 7 and the NEXT rows
-    from paper_2410_22575_b200.build import source_hash
-    src_hash = source_hash()
-    sweep = []
-    algo_fn = {"hvp": chf.hvp_batch, "sym_hvp": chf.sym_hvp_batch, "hvp_hoisted": chf.hvp_batch_hoisted,
-               "hvp_seedsparse": chf.hvp_batch_seedsparse}
-    if not args.no_sweep:
-        for algo, fnb in algo_fn.items():
-            for f in FUNCS:
-                for c in (1, 2, 4, 8, 16):
-                    if n % c or not chf.is_supported(f, n, c, algo):
-                        continue
-                    for _ in range(3):
-                        fnb(f, pts, vec, c, params[f], out=out)
-                    torch.cuda.synchronize()
-                    barrier()
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    ks = 10
-                    e0.record(stream)
-                    for _ in range(ks):
-                        fnb(f, pts, vec, c, params[f], out=out)
-                    e1.record(stream)
-                    torch.cuda.synchronize()
-                    tt = max_over_ranks(e0.elapsed_time(e1) / 1e3) / ks
-                    fl = chf.model_flops_per_point(f, n, c, algo=algo)
-                    exs = executed_entry(f, n, c, src_hash, algo)
-                    sweep.append({"algo": algo, "func": f, "csize": c, "hvp_per_s": m_all / tt, "ms": tt * 1e3,
-                                  "model_tflops_effective": m * fl / tt / 1e12,
-                                  "executed_tflops": None if exs is None else
-                                  m * exs["executed_flops_per_point"] / tt / 1e12,
-                                  "executed_frac": None if exs is None else
-                                  m * exs["executed_flops_per_point"] / tt / 1e12 / peak_tf})
+    # ---- cfg5 (BASELINE configs[4]): 2^23 points sharded over the ranks, compute-only and
+    # compute + all-gather of the results (NCCL all_gather_into_tensor into one buffer)
+    strong = None
+    if not args.no_strong and not args.m_total:
+        f5, c5 = shard(CFG5_M_TOTAL, rank, world)
+        gb = GatherBuffer(CFG5_M_TOTAL, (n,), torch.float64, dev)
+        p5 = torch.from_numpy(synth.points(0, n, c5, f5)).to(dev)
+        v5 = torch.from_numpy(synth.vectors(0, n, c5, f5)).to(dev)
+        o5 = gb.local(rank)
+        ks = 10
+        tc, _ = timed_steps(lambda: chf.hvp_batch(args.func, p5, v5, C, params[args.func], out=o5), ks, 3)
+        tg, _ = timed_steps(lambda: (chf.hvp_batch(args.func, p5, v5, C, params[args.func], out=o5), gb.gather()),
+                            ks, 3)
+        tc, tg = max_over_ranks(tc) / ks, max_over_ranks(tg) / ks
+        res = gb.result()
+        ok = None
+        if rank == 0:  # gathered rows of every rank's shard agree with a direct evaluation
+            import oracle
+            chk = np.unique(np.concatenate([[0, CFG5_M_TOTAL - 1], np.arange(0, CFG5_M_TOTAL, CFG5_M_TOTAL // 97)]))
+            ref, sabs = oracle.hvp_batch(args.func, synth.points(0, n, CFG5_M_TOTAL)[chk],
+                                         synth.vectors(0, n, CFG5_M_TOTAL)[chk], C, params_np[args.func])
+            ok = bool(oracle.componentwise_error(res[chk].cpu().numpy(), ref, sabs).max() <= 1e-10)
+        strong = {"workload": f"cfg5: {args.func} n={n} C={C} m={CFG5_M_TOTAL} over {world} GPU(s)",
+                  "value": CFG5_M_TOTAL / tc, "ms": tc * 1e3, "value_with_gather": CFG5_M_TOTAL / tg,
+                  "ms_with_gather": tg * 1e3, "gather": gb.kind, "gather_parity": ok}
+        del gb, p5, v5, o5, res
 
-    # ---- the paper's own Fig. 2 L2 kernel design recompiled for sm_100a (comparison baseline)
-    paper_l2 = None
-    if not args.no_sweep and args.func in ("rosenbrock", "prodsum") and n in (2, 4, 8, 16):
-        best = None
-        for c in (1, 2, 4, 8, 16):
-            if n % c:
-                continue
-            try:
-                chf.hvp_batch_paper_l2(args.func, pts, vec, c, out=out)
-            except chf.ChessfadError:
-                continue
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(5):
-                chf.hvp_batch_paper_l2(args.func, pts, vec, c, out=out)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            tt = max_over_ranks(e0.elapsed_time(e1) / 1e3) / 5
-            if best is None or tt < best[1]:
-                best = (c, tt)
-        if best:
-            paper_l2 = {"kernel": "paper Fig. 2 L2 design (thread per instance x row x chunk, per-thread hDual y[n], "
-                                  "shared-memory reduction), recompiled for sm_100a", "best_csize": best[0],
-                        "hvp_per_s": m_all / best[1], "ms": best[1] * 1e3, "ours_over_paper_l2": best[1] / per_step}
+    # ---- chunk sweep over the four functions (cfg2), Alg 7 and the NEXT rows -> sweep file
+    sweep, paper_l2 = [], None
+    if not args.no_sweep and world == 1:
+        sweep, paper_l2 = run_sweep(chf, args, pts, vec, out, params, stream, m, m_all, peak_tf, per_step,
+                                    timed_steps, max_over_ranks)
 
     # ---- CPU baseline: the oracle on the host cores, rank 0 at N=1 only
     cpu = None
@@ -363,62 +392,99 @@ def main():
         threads = oracle.default_threads()
         rate, ms, dt = oracle_rate(args.func, n, C, params_np[args.func], 0, 12.0, threads)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": f"{ms} points (first {ms} of the seeded cfg2 stream), {dt:.1f} s of Alg 7 in the plain C "
-                         f"oracle, {threads} pthreads"}
+               "sample": f"first {ms} points of the cfg2 stream: {dt:.1f} s of Alg 7 in the plain C oracle, "
+                         f"{threads} pthreads"}
 
-    # executed FP64 FLOPs of this build, measured by ncu (profiles/executed_flops.json)
+    # ---- roofline: executed FP64 FLOPs of this build (ncu, profiles/executed_flops.json)
     from paper_2410_22575_b200.build import source_hash
     ex = executed_entry(args.func, n, C, source_hash())
-    model_tf = achieved_tf
-    if ex is not None:
-        exec_tf = m * ex["executed_flops_per_point"] / per_step / 1e12
-        traffic = ex["dram_bytes_per_launch"] * m / ex["m"]
-        accounting = ("executed FP64 FLOPs (2*DFMA+DMUL+DADD per point; " + ex["basis"] + ") x m / event time; "
-                      "model FLOPs reported as model_tflops_effective")
-    else:
-        exec_tf, traffic = None, None
-        accounting = "executed-FLOP table missing or stale for this build: achieved = model FLOPs (effective)"
+    exec_tf = None if ex is None else m * ex["executed_flops_per_point"] / per_step / 1e12
+    traffic = None if ex is None else ex["dram_bytes_per_launch"] * m / ex["m"]
     achieved = exec_tf if exec_tf is not None else model_tf
-
-    gather = None
-    if args.gather:
-        torch.cuda.synchronize()
-        barrier()
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        g0.record(stream)
-        full = gather_rows(out, m_all)
-        g1.record(stream)
-        torch.cuda.synchronize()
-        gather = {"ms": max_over_ranks(g0.elapsed_time(g1)), "bytes_per_rank": int(full.numel() * 8),
-                  "collective": "all_gather (NCCL)" if world > 1 else "none (1 rank)"}
-        del full
+    alg_bytes = 24 * n * m  # a1 + a7: read points and vectors, write out (§8(d))
 
     if rank == 0:
+        sweep_best = {}
+        for r in sweep:
+            if r["algo"] == "hvp" and r["hvp_per_s"] > sweep_best.get(r["func"], [0, 0])[1]:
+                sweep_best[r["func"]] = [r["csize"], r["hvp_per_s"]]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
-            "scaling": "strong" if args.m_total else "weak",
+            "warmup": args.warmup, "ms_per_step": per_step * 1e3,
+            "step_ms": {"median": step_med * 1e3, "best": step_best * 1e3, "samples": args.steps},
+            "higher_is_better": True, "scaling": "strong" if args.m_total else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_config(args, world),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf, "traffic": traffic, "accounting": accounting,
-                         "model_tflops_effective": model_tf, "model_frac_effective": model_tf / peak_tf,
-                         "executed_flops_per_point": None if ex is None else ex["executed_flops_per_point"],
-                         "fp64_pipe_active_pct_ncu": None if ex is None else ex["fp64_pipe_active_pct"],
-                         "kernel": f"hvp_reg_kernel<{args.func},C={C}>" if args.func != "fletcher_powell"
-                         else "hvp_f3_kernel",
-                         "peak_basis": f"derived: {SMS} SMs x {FP64_FMA_PER_SM_CLK} FP64 FMA/clk x 2 x {peak_mhz:.0f} MHz "
-                                       "(sm_max_mhz, MEASURED_PEAKS.json); DESIGN.md",
-                         "model_flops_per_point": flops_pt,
-                         "fp64_probe_tflops": probe_tf, "frac_of_probe": achieved / probe_tf},
+                         "frac": achieved / peak_tf,
+                         "frac_executed": None if exec_tf is None else exec_tf / peak_tf,
+                         "frac_model": model_tf / peak_tf, "achieved_model": model_tf,
+                         "executed_over_model": None if ex is None else ex["executed_flops_per_point"] / flops_pt,
+                         "model_flops_per_point": flops_pt, "traffic": traffic, "algorithmic_bytes": alg_bytes,
+                         "hbm_gbs": alg_bytes / per_step / 1e9,
+                         "fp64_pipe_pct_ncu": None if ex is None else ex["fp64_pipe_active_pct"],
+                         "basis": ("frac = executed FP64 FLOPs (ncu 2*DFMA+DMUL+DADD, " +
+                                   (ex["basis"] if ex else "missing") + ") / derived peak; frac_model = §8(d) "
+                                   "model FLOPs (nvcc folds 0/1 seed products, so model > executed)"),
+                         "peak_basis": f"derived {SMS} SM x {FP64_FMA_PER_SM_CLK} FMA/clk x 2 x {peak_mhz:.0f} MHz",
+                         "fp64_probe_tflops": probe_tf},
             "cpu_baseline": cpu, "e2e": e2e,
-            # one kernel per call; F3 with n > 32 adds the (A, B) interleave kernel
-            "gpu_launches": args.steps * (2 if (args.func == "fletcher_powell" and n > 32) else 1), "clocks": clocks, "parity": parity,
-            "gather": gather, "paper_l2_baseline": paper_l2, "sweep": sweep,
+            "gpu_launches": args.steps, "clocks": clocks, "parity": parity, "strong": strong,
+            "sweep_best_hvp": sweep_best,
+            "paper_l2_speedup": None if paper_l2 is None else paper_l2["ours_over_paper_l2"],
+            "sweep_file": os.path.relpath(args.sweep_out, ROOT) if sweep else None,
         }
-        print(json.dumps(line), flush=True)
+        if sweep:
+            os.makedirs(os.path.dirname(args.sweep_out), exist_ok=True)
+            with open(args.sweep_out, "w") as f:
+                json.dump({"headline": line, "sweep": sweep, "paper_l2_baseline": paper_l2}, f, indent=1)
+        print(json.dumps(line, separators=(",", ":")), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def run_sweep(chf, args, pts, vec, out, params, stream, m, m_all, peak_tf, per_step, timed_steps, max_over_ranks):
+    """Every (algo, func, C) at the cfg2 shape, plus the paper's own Fig. 2 L2 kernel design."""
+    from paper_2410_22575_b200.build import source_hash
+    src_hash = source_hash()
+    n = args.n
+    sweep = []
+    algo_fn = {"hvp": chf.hvp_batch, "sym_hvp": chf.sym_hvp_batch, "hvp_hoisted": chf.hvp_batch_hoisted,
+               "hvp_seedsparse": chf.hvp_batch_seedsparse}
+    for algo, fnb in algo_fn.items():
+        for f in FUNCS:
+            for c in (1, 2, 4, 8, 16):
+                if n % c or not chf.is_supported(f, n, c, algo):
+                    continue
+                ks = 10
+                tt, per = timed_steps(lambda: fnb(f, pts, vec, c, params[f], out=out), ks, 3)
+                tt = max_over_ranks(tt) / ks
+                fl = chf.model_flops_per_point(f, n, c, algo=algo)
+                exs = executed_entry(f, n, c, src_hash, algo)
+                ex_tf = None if exs is None else m * exs["executed_flops_per_point"] / tt / 1e12
+                sweep.append({"algo": algo, "func": f, "csize": c, "hvp_per_s": m_all / tt, "ms": tt * 1e3,
+                              "ms_median": float(np.median(per)) * 1e3, "ms_best": min(per) * 1e3,
+                              "model_tflops_effective": m * fl / tt / 1e12, "executed_tflops": ex_tf,
+                              "executed_frac": None if ex_tf is None else ex_tf / peak_tf})
+    paper_l2 = None
+    if args.func in ("rosenbrock", "prodsum") and n in (2, 4, 8, 16):
+        best = None
+        for c in (1, 2, 4, 8, 16):
+            if n % c:
+                continue
+            try:
+                chf.hvp_batch_paper_l2(args.func, pts, vec, c, out=out)
+            except chf.ChessfadError:
+                continue
+            tt, _ = timed_steps(lambda: chf.hvp_batch_paper_l2(args.func, pts, vec, c, out=out), 5, 1)
+            tt = max_over_ranks(tt) / 5
+            if best is None or tt < best[1]:
+                best = (c, tt)
+        if best:
+            paper_l2 = {"kernel": "paper Fig. 2 L2 design (thread per instance x row x chunk, per-thread hDual y[n], "
+                                  "shared-memory reduction), recompiled for sm_100a", "best_csize": best[0],
+                        "hvp_per_s": m_all / best[1], "ms": best[1] * 1e3, "ours_over_paper_l2": best[1] / per_step}
+    return sweep, paper_l2
 
 
 def executed_entry(func, n, C, src_hash, algo="hvp", path=None):

@@ -162,6 +162,25 @@ int chessfad_hvp_batch_host(int func, int n, int csize, int64_t m, const double 
                             size_t workspace_bytes, void *stream);
 
 /*
+ * Reusable host-pipeline context: the three streams and the events of
+ * chessfad_hvp_batch_host, created once (on the current device) instead of per call.
+ * create: *ctx = new context or NULL on failure (ERR_ARG if ctx is NULL, ERR_CUDA if a stream
+ * or event cannot be created).  destroy: releases it (NULL is a no-op); the caller must not
+ * destroy a context while a call on it is running.  A context serves one call at a time.
+ */
+typedef struct chessfad_host_ctx chessfad_host_ctx;
+int chessfad_host_ctx_create(chessfad_host_ctx **ctx);
+int chessfad_host_ctx_destroy(chessfad_host_ctx *ctx);
+
+/*
+ * chessfad_hvp_batch_host on a context (same arguments, semantics and errors); ERR_ARG if ctx
+ * is NULL or was created on another device than the current one.
+ */
+int chessfad_hvp_batch_host_ctx(chessfad_host_ctx *ctx, int func, int n, int csize, int64_t m,
+                                const double *points, const double *vecs, double *out, const double *params,
+                                int64_t piece_points, void *workspace, size_t workspace_bytes, void *stream);
+
+/*
  * COMPARISON BASELINE, not the product path: the paper's own GPU design, Fig. 2 "L2"
  * recompiled for sm_100a -- one thread per (instance, row, chunk), a
  * materialised per-thread hDual<C> y[n] seed array, partial dots reduced through shared

@@ -25,7 +25,8 @@ EXPORTS = sorted(["chessfad_hvp_batch", "chessfad_hessian_batch", "chessfad_sym_
                   "chessfad_status_string", "chessfad_model_flops_per_point", "chessfad_model_flops_per_point_algo",
                   "chessfad_fp64_probe", "chessfad_version", "chessfad_hvp_host_workspace_bytes",
                   "chessfad_hvp_batch_hoisted", "chessfad_hvp_batch_seedsparse", "chessfad_hessian_batch_seedsparse", "chessfad_hvp_batch_paper_l2", "chessfad_hessian_grad_batch",
-                  "chessfad_hvp_batch_paper"])
+                  "chessfad_hvp_batch_paper", "chessfad_host_ctx_create", "chessfad_host_ctx_destroy",
+                  "chessfad_hvp_batch_host_ctx"])
 
 _lock = threading.Lock()
 _lib = None
@@ -65,6 +66,10 @@ def load(build_if_missing: bool = True):
             "chessfad_model_flops_per_point_algo": (dbl, [i32, i32, i32, i32]),
             "chessfad_hvp_batch_host": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, i64, vp, ctypes.c_size_t, vp]),
             "chessfad_hvp_host_workspace_bytes": (ctypes.c_size_t, [i32, i32, i64, i64]),
+            "chessfad_host_ctx_create": (i32, [ctypes.POINTER(vp)]),
+            "chessfad_host_ctx_destroy": (i32, [vp]),
+            "chessfad_hvp_batch_host_ctx": (i32, [vp, i32, i32, i32, i64, vp, vp, vp, vp, i64, vp, ctypes.c_size_t,
+                                                  vp]),
             "chessfad_is_supported": (i32, [i32, i32, i32]),
             "chessfad_status_string": (ctypes.c_char_p, [i32]),
             "chessfad_model_flops_per_point": (dbl, [i32, i32, i32, i32]),
@@ -105,24 +110,42 @@ def _dev(t, name, shape=None):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _params_shape(func, n):
+    """Fletcher-Powell params: [A (n x n) | B (n x n) | E* (n)] = 2n^2+n doubles; else ignored."""
+    return (2 * n * n + n,) if _func(func) == FLETCHER_POWELL else None
+
+
+def _dev_params(params, func, n):
+    shp = _params_shape(func, n)
+    if params is not None and shp is not None and params.numel() != shp[0]:
+        raise ValueError(f"params has {params.numel()} elements, expected 2n^2+n = {shp[0]}")
+    return _dev(params, "params")
+
+
+def _points_2d(points):
+    if points.dim() != 2:
+        raise ValueError(f"points must be (m, n), got shape {tuple(points.shape)}")
+    return points.shape
+
+
 def _hvp(entry, func, points, vecs, csize, params, out, stream):
     import torch
-    m, n = points.shape
+    m, n = _points_2d(points)
     if out is None:
         out = torch.empty_like(points)
     st = getattr(load(), entry)(_func(func), n, csize, m, _dev(points, "points"), _dev(vecs, "vecs", (m, n)),
-                                _dev(out, "out", (m, n)), _dev(params, "params"), _stream_ptr(stream))
+                                _dev(out, "out", (m, n)), _dev_params(params, func, n), _stream_ptr(stream))
     _check(st)
     return out
 
 
 def _hess(entry, func, points, csize, params, out, stream):
     import torch
-    m, n = points.shape
+    m, n = _points_2d(points)
     if out is None:
         out = torch.empty((m, n, n), dtype=torch.float64, device=points.device)
     st = getattr(load(), entry)(_func(func), n, csize, m, _dev(points, "points"), _dev(out, "hess", (m, n, n)),
-                                _dev(params, "params"), _stream_ptr(stream))
+                                _dev_params(params, func, n), _stream_ptr(stream))
     _check(st)
     return out
 
@@ -185,14 +208,14 @@ def hessian_batch(func, points, csize: int, params=None, out=None, stream=None):
 def hessian_grad_batch(func, points, csize: int, params=None, out=None, grad=None, stream=None):
     """(hess, grad): Alg 5 Hessians plus the gradient by-product from slot v[1]."""
     import torch
-    m, n = points.shape
+    m, n = _points_2d(points)
     if out is None:
         out = torch.empty((m, n, n), dtype=torch.float64, device=points.device)
     if grad is None:
         grad = torch.empty((m, n), dtype=torch.float64, device=points.device)
     st = load().chessfad_hessian_grad_batch(_func(func), n, csize, m, _dev(points, "points"),
                                             _dev(out, "hess", (m, n, n)), _dev(grad, "grad", (m, n)),
-                                            _dev(params, "params"), _stream_ptr(stream))
+                                            _dev_params(params, func, n), _stream_ptr(stream))
     _check(st)
     return out, grad
 
@@ -208,7 +231,10 @@ def sym_hessian_batch(func, points, csize: int, params=None, out=None, stream=No
     return _hess("chessfad_sym_hessian_batch", func, points, csize, params, out, stream)
 
 
-def _host_ptr(x, name, writable=False):
+def _host_arr(x, name, shape, writable=False):
+    """(pointer, owner) of a contiguous float64 HOST buffer of exactly `shape`; the owner must
+    stay referenced until the library call returns (a converted copy would otherwise be
+    freed under the call)."""
     import numpy as np
     import torch
     if x is None:
@@ -216,34 +242,81 @@ def _host_ptr(x, name, writable=False):
     if isinstance(x, torch.Tensor):
         if x.is_cuda or x.dtype != torch.float64 or not x.is_contiguous():
             raise TypeError(f"{name} must be a contiguous float64 CPU tensor")
-        return ctypes.c_void_p(x.data_ptr()), x
-    a = np.asarray(x)
-    if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"] or (writable and not a.flags["WRITEABLE"]):
-        raise TypeError(f"{name} must be a contiguous writable float64 array")
-    return ctypes.c_void_p(a.ctypes.data), a
+        ptr, shp = x.data_ptr(), tuple(x.shape)
+    else:
+        if writable and not isinstance(x, np.ndarray):
+            raise TypeError(f"{name} must be a numpy array or a CPU tensor (written in place)")
+        x = np.asarray(x)
+        if x.dtype != np.float64 or not x.flags["C_CONTIGUOUS"] or (writable and not x.flags["WRITEABLE"]):
+            raise TypeError(f"{name} must be a contiguous{' writable' if writable else ''} float64 array")
+        ptr, shp = x.ctypes.data, tuple(x.shape)
+    if shp != tuple(shape) and not (len(shape) == 1 and int(np.prod(shp)) == shape[0]):
+        raise ValueError(f"{name} has shape {shp}, expected {tuple(shape)}")
+    return ctypes.c_void_p(ptr), x
+
+
+class HostPipeline:
+    """End-to-end HVP on HOST buffers through one reusable chessfad_host_ctx (streams and
+    events created once) and a cached device workspace from torch's allocator."""
+
+    def __init__(self):
+        self._lib = load()
+        h = ctypes.c_void_p()
+        _check(self._lib.chessfad_host_ctx_create(ctypes.byref(h)))
+        self._ctx = h
+        self._ws = None
+
+    def close(self):
+        if self._ctx is not None:
+            self._lib.chessfad_host_ctx_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def hvp(self, func, points, vecs, csize: int, params=None, out=None, piece_points: int = 0, stream=None):
+        return _host_call(self._lib, self._ctx, self, func, points, vecs, csize, params, out, piece_points, stream,
+                          None)
+
+
+def _host_call(lib, ctx, holder, func, points, vecs, csize, params, out, piece_points, stream, workspace):
+    import numpy as np
+    import torch
+    shp = np.shape(points)
+    if len(shp) != 2:
+        raise ValueError(f"points must be (m, n), got shape {tuple(shp)}")
+    m, n = shp
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float64, pin_memory=torch.cuda.is_available())
+    pp, k0 = _host_arr(points, "points", (m, n))
+    pv, k1 = _host_arr(vecs, "vecs", (m, n))
+    po, k2 = _host_arr(out, "out", (m, n), writable=True)
+    pshape = _params_shape(func, n)
+    ppar, k3 = _host_arr(params, "params", pshape) if pshape is not None else (None, None)
+    need = lib.chessfad_hvp_host_workspace_bytes(_func(func), n, m, piece_points)
+    ws = workspace if workspace is not None else (holder._ws if holder is not None else None)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 1), dtype=torch.uint8, device="cuda")
+        if holder is not None:
+            holder._ws = ws
+    args = (_func(func), n, csize, m, pp, pv, po, ppar, piece_points, ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+            _stream_ptr(stream))
+    st = lib.chessfad_hvp_batch_host_ctx(ctx, *args) if ctx is not None else lib.chessfad_hvp_batch_host(*args)
+    del k0, k1, k2, k3  # kept alive across the call
+    _check(st)
+    return out
 
 
 def hvp_batch_host(func, points, vecs, csize: int, params=None, out=None, piece_points: int = 0, stream=None,
                    workspace=None):
     """End-to-end HVP on HOST buffers (numpy arrays or CPU tensors, ideally pinned): H2D
     copies, kernels and D2H copies in a three-stage stream pipeline; synchronous.  The device
-    workspace comes from torch's caching allocator (or `workspace`, a CUDA uint8 tensor)."""
-    import torch
-    m, n = points.shape
-    if out is None:
-        out = torch.empty((m, n), dtype=torch.float64, pin_memory=torch.cuda.is_available())
-    pp, _ = _host_ptr(points, "points")
-    pv, _ = _host_ptr(vecs, "vecs")
-    po, _ = _host_ptr(out, "out", writable=True)
-    ppar, _ = _host_ptr(params, "params")
-    lib = load()
-    need = lib.chessfad_hvp_host_workspace_bytes(_func(func), n, m, piece_points)
-    if workspace is None or workspace.numel() < need:
-        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device="cuda")
-    st = lib.chessfad_hvp_batch_host(_func(func), n, csize, m, pp, pv, po, ppar, piece_points,
-                                     ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _stream_ptr(stream))
-    _check(st)
-    return out
+    workspace comes from torch's caching allocator (or `workspace`, a CUDA uint8 tensor).
+    HostPipeline reuses the streams/events across calls."""
+    return _host_call(load(), None, None, func, points, vecs, csize, params, out, piece_points, stream, workspace)
 
 
 def is_supported(func, n: int, csize: int, algo: str | None = None) -> bool:

@@ -70,10 +70,21 @@ def _compile(src: str, defines=(), tag: str = "") -> str:
 
 
 def build(force: bool = False, jobs: int | None = None, defines=(), out: str | None = None) -> str:
-    """Build the library; `defines`/`out` build an experimental variant elsewhere (tuning)."""
+    """Build the library; `defines`/`out` build an experimental variant elsewhere (tuning).
+    Serialised across processes by an fcntl lock on build/.lock (concurrent ranks would
+    otherwise write the same object files); a process that waited re-checks staleness."""
     if not force and not defines and out is None and up_to_date():
         return LIB
+    import fcntl
     os.makedirs(BUILD, exist_ok=True)
+    with open(os.path.join(BUILD, ".lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if not force and not defines and out is None and up_to_date():
+            return LIB
+        return _build_locked(jobs, defines, out)
+
+
+def _build_locked(jobs, defines, out) -> str:
     srcs = sources()
     tag = "_" + "_".join(d.replace("=", "") for d in defines) if defines else ""
     with cf.ThreadPoolExecutor(max_workers=jobs or min(len(srcs), os.cpu_count() or 4)) as ex:

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <new>
 
 #include "../../include/chessfad.h"
 #include "launch.cuh"
@@ -159,7 +160,10 @@ template <int MODE>
 cudaError_t dispatch_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s) {
   const int C = reg_kernel_chunk(Capi);
   if constexpr (MODE == MODE_HVP_ROWHOIST) {  // NEXT-4 (chessfad_hvp_batch_hoisted), register path
-    if (a.n == 2 || a.n == 4 || a.n == 8 || a.n == 16) {
+    // the compile-time kernels use 16-byte double2 loads/stores of whole point rows
+    const bool aligned = ((reinterpret_cast<uintptr_t>(a.points) | reinterpret_cast<uintptr_t>(a.vecs) |
+                           reinterpret_cast<uintptr_t>(a.out)) & 15) == 0;
+    if (aligned && (a.n == 2 || a.n == 4 || a.n == 8 || a.n == 16)) {
       switch (func) {
         case CHESSFAD_ROSENBROCK: return dispatch_small<FUNC_ROSENBROCK>(C, a, s);
         case CHESSFAD_ACKLEY: return dispatch_small<FUNC_ACKLEY>(C, a, s);
@@ -306,42 +310,73 @@ size_t chessfad_hvp_host_workspace_bytes(int func, int n, int64_t m, int64_t pie
   return host_ws_bytes(func, n, m, piece_points);
 }
 
+}  // extern "C"
+
+// Streams and events of the host-buffer pipeline: created once per chessfad_host_ctx and
+// reused by every call on it (chessfad_hvp_batch_host makes a temporary one).
+struct chessfad_host_ctx {
+  enum { H2D = 0, KRN = 1, D2H = 2 };
+  cudaStream_t ss[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ready = nullptr, ev[3][kHostSets] = {};
+  int device = -1;
+  cudaError_t init() {
+    cudaError_t e = cudaGetDevice(&device);
+    for (int k = 0; k < 3 && e == cudaSuccess; k++) e = cudaStreamCreateWithFlags(&ss[k], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+    for (int k = 0; k < 3; k++)
+      for (int b = 0; b < kHostSets && e == cudaSuccess; b++) e = cudaEventCreateWithFlags(&ev[k][b], cudaEventDisableTiming);
+    return e;
+  }
+  ~chessfad_host_ctx() {
+    for (int k = 0; k < 3; k++) {
+      if (ss[k]) cudaStreamDestroy(ss[k]);
+      for (int b = 0; b < kHostSets; b++)
+        if (ev[k][b]) cudaEventDestroy(ev[k][b]);
+    }
+    if (ready) cudaEventDestroy(ready);
+  }
+};
+
+namespace {
 // Three-stage pipeline over pieces of the batch: an H2D stream copies piece p into buffer set
 // p % 3 (after that set's previous D2H), a compute stream runs the kernel, a D2H stream copies
 // the result back -- the H2D copy engine never waits for a kernel, H2D and D2H overlap.
-int chessfad_hvp_batch_host(int func, int n, int csize, int64_t m, const double* points, const double* vecs,
-                            double* out, const double* params, int64_t piece_points, void* workspace,
-                            size_t workspace_bytes, void* stream) {
+// argument checks of the host-buffer entry points (no CUDA call)
+int host_precheck(int func, int n, int csize, int64_t m, const double* points, const double* vecs, double* out,
+                  const double* params, int64_t piece_points, void* workspace, size_t workspace_bytes) {
   int st = validate(func, n, csize, m, false, params, points, vecs, out);
   if (st) return st;
   if (!supported(func, n, csize, MODE_HVP)) return CHESSFAD_ERR_UNSUPPORTED;
-  if (m == 0) return CHESSFAD_OK;
+  if (m > 0 && workspace && workspace_bytes < host_ws_bytes(func, n, m, piece_points)) return CHESSFAD_ERR_ARG;
+  return CHESSFAD_OK;
+}
+
+int host_pipeline(chessfad_host_ctx* cx, int func, int n, int csize, int64_t m, const double* points,
+                  const double* vecs, double* out, const double* params, int64_t piece_points, void* workspace,
+                  size_t workspace_bytes, void* stream) {
+  int st = host_precheck(func, n, csize, m, points, vecs, out, params, piece_points, workspace, workspace_bytes);
+  if (st || m == 0) return st;
   const size_t need = host_ws_bytes(func, n, m, piece_points);
-  if (workspace && workspace_bytes < need) return CHESSFAD_ERR_ARG;
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev != cx->device) return CHESSFAD_ERR_ARG;
   cudaStream_t s0 = (cudaStream_t)stream;
   const int64_t piece = host_piece(m, piece_points);
   const int npieces = (int)((m + piece - 1) / piece);
   const size_t row = (size_t)n * sizeof(double);
   const size_t pdoubles = (size_t)piece * n;
   const size_t nparams = (func == CHESSFAD_FLETCHER_POWELL) ? (size_t)2 * n * n + n : 0;
-
   enum { H2D = 0, KRN = 1, D2H = 2 };
-  cudaStream_t ss[3] = {nullptr, nullptr, nullptr};
-  cudaEvent_t ready = nullptr, ev[3][kHostSets] = {};
+  cudaStream_t* ss = cx->ss;
   double* d_buf = (double*)workspace;
   const bool own = d_buf == nullptr;
   cudaError_t e = cudaSuccess;
   auto ok = [&](cudaError_t x) { if (e == cudaSuccess) e = x; return e == cudaSuccess; };
-  for (int k = 0; k < 3; k++) ok(cudaStreamCreateWithFlags(&ss[k], cudaStreamNonBlocking));
-  ok(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-  for (int k = 0; k < 3; k++)
-    for (int b = 0; b < kHostSets; b++) ok(cudaEventCreateWithFlags(&ev[k][b], cudaEventDisableTiming));
   if (own) ok(cudaMallocAsync((void**)&d_buf, need, s0));
   if (e == cudaSuccess) {
     double* d_params = d_buf + (size_t)kHostSets * 3 * pdoubles;
     if (nparams) ok(cudaMemcpyAsync(d_params, params, nparams * sizeof(double), cudaMemcpyHostToDevice, s0));
-    ok(cudaEventRecord(ready, s0));
-    for (int k = 0; k < 3; k++) ok(cudaStreamWaitEvent(ss[k], ready, 0));
+    ok(cudaEventRecord(cx->ready, s0));
+    for (int k = 0; k < 3; k++) ok(cudaStreamWaitEvent(ss[k], cx->ready, 0));
     for (int p = 0; p < npieces && e == cudaSuccess; p++) {
       const int b = p % kHostSets;
       double* dp = d_buf + (size_t)(3 * b) * pdoubles;
@@ -350,34 +385,72 @@ int chessfad_hvp_batch_host(int func, int n, int csize, int64_t m, const double*
       const int64_t e0 = (int64_t)p * piece;
       const int64_t cnt = std::min(piece, m - e0);
       const size_t bytes = (size_t)cnt * row;
-      if (p >= kHostSets) ok(cudaStreamWaitEvent(ss[H2D], ev[D2H][b], 0));  // set b drained
+      if (p >= kHostSets) ok(cudaStreamWaitEvent(ss[H2D], cx->ev[D2H][b], 0));  // set b drained
       ok(cudaMemcpyAsync(dp, points + e0 * n, bytes, cudaMemcpyHostToDevice, ss[H2D]));
       ok(cudaMemcpyAsync(dv, vecs + e0 * n, bytes, cudaMemcpyHostToDevice, ss[H2D]));
-      ok(cudaEventRecord(ev[H2D][b], ss[H2D]));
-      ok(cudaStreamWaitEvent(ss[KRN], ev[H2D][b], 0));
+      ok(cudaEventRecord(cx->ev[H2D][b], ss[H2D]));
+      ok(cudaStreamWaitEvent(ss[KRN], cx->ev[H2D][b], 0));
       if (e == cudaSuccess) {
         const int r = run<MODE_HVP>(func, n, csize, cnt, dp, dv, dout, nparams ? d_params : nullptr, ss[KRN]);
         if (r != CHESSFAD_OK) e = cudaErrorLaunchFailure;
       }
-      ok(cudaEventRecord(ev[KRN][b], ss[KRN]));
-      ok(cudaStreamWaitEvent(ss[D2H], ev[KRN][b], 0));
+      ok(cudaEventRecord(cx->ev[KRN][b], ss[KRN]));
+      ok(cudaStreamWaitEvent(ss[D2H], cx->ev[KRN][b], 0));
       ok(cudaMemcpyAsync(out + e0 * n, dout, bytes, cudaMemcpyDeviceToHost, ss[D2H]));
-      ok(cudaEventRecord(ev[D2H][b], ss[D2H]));
+      ok(cudaEventRecord(cx->ev[D2H][b], ss[D2H]));
     }
-    for (int k = 0; k < 3; k++) {
-      ok(cudaEventRecord(ready, ss[k]));
-      ok(cudaStreamWaitEvent(s0, ready, 0));
+    for (int k = 0; k < 3; k++) {  // s0 joins all three streams
+      ok(cudaEventRecord(cx->ready, ss[k]));
+      ok(cudaStreamWaitEvent(s0, cx->ready, 0));
     }
     if (own) ok(cudaFreeAsync(d_buf, s0));
-    ok(cudaStreamSynchronize(s0));
   }
-  for (int k = 0; k < 3; k++) {
-    if (ss[k]) cudaStreamDestroy(ss[k]);
-    for (int b = 0; b < kHostSets; b++)
-      if (ev[k][b]) cudaEventDestroy(ev[k][b]);
-  }
-  if (ready) cudaEventDestroy(ready);
+  const cudaError_t es = cudaStreamSynchronize(s0);
+  if (e == cudaSuccess) e = es;
   return e == cudaSuccess ? CHESSFAD_OK : CHESSFAD_ERR_CUDA;
+}
+}  // namespace
+
+extern "C" {
+
+int chessfad_host_ctx_create(chessfad_host_ctx** ctx) {
+  if (!ctx) return CHESSFAD_ERR_ARG;
+  *ctx = nullptr;
+  chessfad_host_ctx* c = new (std::nothrow) chessfad_host_ctx();
+  if (!c) return CHESSFAD_ERR_CUDA;
+  if (c->init() != cudaSuccess) {
+    delete c;
+    return CHESSFAD_ERR_CUDA;
+  }
+  *ctx = c;
+  return CHESSFAD_OK;
+}
+
+int chessfad_host_ctx_destroy(chessfad_host_ctx* ctx) {
+  delete ctx;  // NULL is a no-op
+  return CHESSFAD_OK;
+}
+
+int chessfad_hvp_batch_host_ctx(chessfad_host_ctx* ctx, int func, int n, int csize, int64_t m, const double* points,
+                                const double* vecs, double* out, const double* params, int64_t piece_points,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+  if (!ctx) return CHESSFAD_ERR_ARG;
+  return host_pipeline(ctx, func, n, csize, m, points, vecs, out, params, piece_points, workspace, workspace_bytes,
+                       stream);
+}
+
+int chessfad_hvp_batch_host(int func, int n, int csize, int64_t m, const double* points, const double* vecs,
+                            double* out, const double* params, int64_t piece_points, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  int st = host_precheck(func, n, csize, m, points, vecs, out, params, piece_points, workspace, workspace_bytes);
+  if (st || m == 0) return st;
+  chessfad_host_ctx* cx = nullptr;
+  st = chessfad_host_ctx_create(&cx);
+  if (st) return st;
+  st = host_pipeline(cx, func, n, csize, m, points, vecs, out, params, piece_points, workspace, workspace_bytes,
+                     stream);
+  chessfad_host_ctx_destroy(cx);
+  return st;
 }
 
 int chessfad_is_supported(int func, int n, int csize) {

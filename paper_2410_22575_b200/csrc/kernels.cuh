@@ -295,7 +295,9 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? CHF_F3_SMEM_MINB : 2)
   for (int i = warp / G; i < n; i += rstep) {
     const int scn = i / C;
     RowSink<MODE> sink = make_sink<MODE>(p, i, e, v, o, VEC_TILE ? kPad : 1);
-    if (MODE == MODE_HESS_GRAD && e < p.m) {  // gradient: slot 1 of f = sum_k r_k r_k
+    if (MODE == MODE_HESS_GRAD) {  // gradient: slot 1 of f = sum_k r_k r_k
+      // every lane runs phase A (the (A, B) ring is filled and __syncwarp'ed by all 32 lanes;
+      // tail lanes hold a replicated point); only the store is guarded
       if (AB_SMEM)
         f3_phase_a<KB>(n, i, sa, ca, kPad, ABShared{s_ab, n}, Es, R0, R1);
       else
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? CHF_F3_SMEM_MINB : 2)
         const double rr1 = R0[k] * R1[k] + R0[k] * R1[k];  // (r*r)[1] = r0 r1 + r0 r1 (Fig. 1)
         f1 = (k == 0) ? rr1 : f1 + rr1;
       }
-      p.grad[e * n + i] = f1;
+      if (e < p.m) p.grad[e * n + i] = f1;
     }
     if (MODE == MODE_HVP_ROWHOIST) {  // NEXT-4: phase A once per row
       if (AB_SMEM)

@@ -34,16 +34,56 @@ def max_over_ranks(x: float, device=None) -> float:
     return float(t.item())
 
 
+def _world_rank():
+    if not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(), dist.get_rank()
+
+
+class GatherBuffer:
+    """Preallocated result gather for the shard() layout.
+
+    One (world * cmax, *row) buffer holds every rank's slot (cmax = largest shard); the
+    kernel writes this rank's rows straight into its own slot (local()), and gather() is one
+    in-place all_gather_into_tensor (no staging copy, no list of parts, no torch.cat).  When
+    the shards are equal (m_total % world == 0, e.g. cfg5) the buffer IS the gathered
+    result; otherwise result() compacts the padded slots once."""
+
+    def __init__(self, m_total: int, row_shape=(), dtype=torch.float64, device=None):
+        self.world, self.rank = _world_rank()
+        self.m_total = m_total
+        self.shards = all_shards(m_total, self.world)
+        self.cmax = max(c for _, c in self.shards) if m_total else 0
+        self.equal = all(c == self.cmax for _, c in self.shards)
+        self.full = torch.empty((self.world * self.cmax,) + tuple(row_shape), dtype=dtype, device=device)
+        self.kind = "all_gather_into_tensor in place" if self.world > 1 else "none (1 rank)"
+
+    def slot(self, rank: int) -> torch.Tensor:
+        return self.full[rank * self.cmax:(rank + 1) * self.cmax]
+
+    def local(self, rank: int | None = None) -> torch.Tensor:
+        """This rank's output rows (a view into the gather buffer)."""
+        r = self.rank if rank is None else rank
+        return self.slot(r)[: self.shards[r][1]]
+
+    def gather(self) -> None:
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.full, self.slot(self.rank))
+
+    def result(self) -> torch.Tensor:
+        if self.world == 1 or self.equal:
+            return self.full[: self.m_total]
+        return torch.cat([self.slot(r)[:c] for r, (_, c) in enumerate(self.shards)], dim=0)
+
+
 def gather_rows(local: torch.Tensor, m_total: int) -> torch.Tensor:
     """All-gather row shards (shard() layout) into the full (m_total, ...) tensor on every
-    rank.  Shards are padded to the largest count so that one all_gather suffices."""
-    if not dist.is_initialized() or dist.get_world_size() == 1:
+    rank.  Copies `local` into a GatherBuffer slot; write into GatherBuffer.local() directly
+    to avoid that copy."""
+    world, rank = _world_rank()
+    if world == 1:
         return local
-    world = dist.get_world_size()
-    shards = all_shards(m_total, world)
-    cmax = max(c for _, c in shards)
-    pad = torch.zeros((cmax,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
-    pad[: local.shape[0]] = local
-    parts = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(parts, pad)
-    return torch.cat([p[:c] for p, (_, c) in zip(parts, shards)], dim=0)
+    gb = GatherBuffer(m_total, tuple(local.shape[1:]), local.dtype, local.device)
+    gb.local(rank).copy_(local)
+    gb.gather()
+    return gb.result()

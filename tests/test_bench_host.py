@@ -41,3 +41,32 @@ def test_clock_reason_decoding():
     cs.reasons = 0x1 | 0x4 | 0x40
     s = cs.summary()
     assert s["sm_mhz"] == 1965 and s["reasons"] == ["sw_power_cap", "hw_thermal_slowdown"]
+
+
+def test_gpus_flag_respawns_under_torchrun():
+    """`bench.py --gpus 2` outside torchrun re-executes itself with 2 ranks (gloo-free: the
+    reference arm needs no process group); rank 0 alone prints the line, with n_gpus = 2."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "3", "--n", "4", "--csize", "2", "--ref-step-s", "0.05"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference" and d["value"] > 0
+    assert len(lines[0]) < 2048
+
+
+def test_world_size_mismatch_rejected(monkeypatch):
+    import pytest
+    monkeypatch.setenv("WORLD_SIZE", "4")
+    a = bench.parse_args(["--gpus", "2"])
+    with pytest.raises(SystemExit):
+        bench.maybe_respawn(a, ["--gpus", "2"])
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    assert bench.maybe_respawn(a, ["--gpus", "2"]) is None

@@ -13,7 +13,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import synth
-from paper_2410_22575_b200.dist import all_shards, gather_rows, max_over_ranks, shard
+from paper_2410_22575_b200.dist import GatherBuffer, all_shards, gather_rows, max_over_ranks, shard
 
 
 def test_shard_cover():
@@ -53,8 +53,13 @@ def _worker(rank, world, port, m_total, n, q):
     pts = torch.from_numpy(synth.points(0, n, count, first))
     local = pts * 2.0 + 1.0  # stand-in row-local result
     full = gather_rows(local, m_total)
+    # preallocated in-place path: the "kernel" writes straight into this rank's slot
+    gb = GatherBuffer(m_total, (n,), torch.float64)
+    gb.local().copy_(local)
+    gb.gather()
+    full2 = gb.result()
     t = max_over_ranks(0.5 + rank)
-    q.put((rank, full.numpy(), t))
+    q.put((rank, full.numpy(), t, full2.numpy(), gb.kind))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -73,6 +78,7 @@ def test_gloo_world2_gather_and_max(m_total):
         p.join(timeout=60)
         assert p.exitcode == 0
     want = synth.points(0, n, m_total) * 2.0 + 1.0
-    for rank, full, t in res:
+    for rank, full, t, full2, kind in res:
         assert np.array_equal(full, want)
-        assert t == 1.5
+        assert np.array_equal(full2, want)
+        assert t == 1.5 and "all_gather_into_tensor" in kind

@@ -201,18 +201,37 @@ def test_host_api_matches_device_api(chf):
 
 
 # ------------------------------------------------------------ full size, bench launch configuration
+HVP_ENTRIES = {"hvp": "hvp_batch", "sym_hvp": "sym_hvp_batch", "hvp_hoisted": "hvp_batch_hoisted",
+               "hvp_seedsparse": "hvp_batch_seedsparse"}
+
+
 @pytest.mark.parametrize("func", FUNCS)
-def test_full_size_sampled(chf, func):
-    """cfg2 at BASELINE size (n=16, m=2^20) in the bench launch configuration; the oracle
-    checks a deterministic sample (first, last, fixed stride) point by point."""
+def test_cfg2_every_point(chf, func):
+    """cfg2 at BASELINE size (n=16, m=2^20), EVERY point, every C in {1,2,4,8,16} and every HVP
+    entry point (Alg 7 in the bench launch configuration, Alg 8, NEXT-4 hoisted and
+    seed-sparse) against the oracle (computed once: its HVP is bitwise C-invariant,
+    test_oracle_pins.test_chunk_invariance) and against the vectorised closed form
+    (tests/closed_forms_np.py, independent of both)."""
+    from tests import closed_forms_np as cfn
     n, m = 16, 1 << 20
     P, V = synth.points(0, n, m), synth.vectors(0, n, m)
     params = _params(func, n)
-    idx = np.unique(np.concatenate([[0, m - 1], np.arange(0, m, 4099)]))
-    ref, sabs = oracle.hvp_batch(func, P[idx], V[idx], 16, params)
-    for C in (1, 4, 16):
-        got = _gpu_hvp(chf, func, P, V, C, params)
-        _check(got[idx], ref, sabs)
+    ref, sabs = oracle.hvp_batch(func, P, V, 16, params)
+    hv, S = cfn.hvp(func, P, V, params)
+    assert cfn.error(ref, hv, S) <= TIGHT  # the oracle itself at every point
+    dev = torch.device("cuda")
+    p, v = torch.from_numpy(P).to(dev), torch.from_numpy(V).to(dev)
+    pr = None if params is None else torch.from_numpy(params).to(dev)
+    out = torch.empty_like(p)
+    for algo, entry in HVP_ENTRIES.items():
+        for C in (1, 2, 4, 8, 16):
+            if not chf.is_supported(func, n, C, algo):
+                continue
+            out.fill_(np.nan)
+            getattr(chf, entry)(func, p, v, C, pr, out=out)
+            got = out.cpu().numpy()
+            _check(got, ref, sabs)
+            assert cfn.error(got, hv, S) <= TIGHT, (algo, C)
 
 
 # ------------------------------------------------------------ NEXT-1 / NEXT-2: symmetric algorithms
