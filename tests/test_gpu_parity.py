@@ -508,6 +508,26 @@ def test_hessian_grad(chf, func):
         assert np.array_equal(g.cpu().numpy(), want)
 
 
+def test_hessian_grad_f3_ring_ragged(chf):
+    """Fletcher-Powell n > 32 (the cp.async (A, B) ring) with m % 32 != 0: the partial last
+    warp's gradient and Hessian (tail lanes must take part in the ring)."""
+    func, n, m = "fletcher_powell", 64, 45
+    P = synth.points(21, n, m)
+    params = _params(func, n)
+    dev = torch.device("cuda")
+    pr = torch.from_numpy(params).to(dev)
+    ref = [oracle.hessian(func, P[e], params, algo="chunk", C=8) for e in range(m)]
+    ref_H = np.stack([r[0] for r in ref])
+    ref_g = np.stack([r[1] for r in ref])
+    for C in (8, 64):
+        H, g = chf.hessian_grad_batch(func, torch.from_numpy(P).to(dev), C, pr)
+        H, g = H.cpu().numpy(), g.cpu().numpy()
+        gs = np.maximum(np.abs(ref_g).max(axis=1, keepdims=True), 1e-300)
+        assert (np.abs(g - ref_g) / gs).max() <= TIGHT, C
+        hs = np.abs(ref_H).max(axis=(1, 2))
+        assert (np.abs(H - ref_H).max(axis=(1, 2)) / hs).max() <= TIGHT, C
+
+
 # ------------------------------------------------------------ maximum sizes of the compiled set
 def test_maximum_n(chf):
     """Largest n each path accepts: register path n = 256 (Ackley 176),
