@@ -198,11 +198,11 @@ def workload_config(args, world):
         wl = f"cfg5: {args.func} n={args.n} C={args.csize} m={args.m_total} over {world} GPU(s) (strong)"
         gp = args.m_total
     else:
-        wl = f"cfg2: {args.func} n={args.n} C={args.csize} m={args.m} per GPU (BASELINE configs[1])"
+        wl = f"cfg2 (configs[1]): {args.func} n={args.n} C={args.csize} m={args.m}/GPU"
         gp = args.m * world
     return {"workload": wl, "func": args.func, "n": args.n, "csize": args.csize, "m_per_gpu": args.m,
-            "global_points": gp, "seed": 0, "parallelism": f"dp{world} (points sharded, no data-path collective)",
-            "l2": f"no flush: inputs {3 * args.m * args.n * 8 / 2**20:.0f} MiB per step > 126 MB L2"}
+            "global_points": gp, "seed": 0, "parallelism": f"dp{world}",
+            "l2": f"no flush: {3 * args.m * args.n * 8 / 2**20:.0f} MiB/step > L2"}
 
 
 # ------------------------------------------------------------------------- our arm
@@ -323,7 +323,7 @@ def main(argv=None):
         got = out.cpu().numpy()[idx]
         err = oracle.componentwise_error(got, ref, sabs)
         parity = {"max_err": float(err.max()), "points": int(idx.size), "of": m, "bar": 1e-10,
-                  "pass": bool(err.max() <= 1e-10), "metric": "|g-r|/max(|r|, sum_j |H_ij||v_j|)"}
+                  "pass": bool(err.max() <= 1e-10)}
 
     # ---- FP64 probe (attainable DFMA rate on this GPU)
     sink = torch.empty(SMS * 8 * 256, dtype=torch.float64, device=dev)
@@ -349,7 +349,7 @@ def main(argv=None):
     assert torch.equal(Oh, out.cpu()), "host-buffer path disagrees with the device path"
     e2e = {"value": m_all / e2e_t, "unit": UNIT, "h2d_bytes_per_step": 2 * m * n * 8 + (
         0 if ph_params is None else ph_params.numel() * 8), "d2h_bytes_per_step": m * n * 8,
-        "ms_per_step": e2e_t * 1e3, "api": "chessfad_hvp_batch_host (pinned; H2D/kernel/D2H stream pipeline)"}
+        "ms_per_step": e2e_t * 1e3, "api": "chessfad_hvp_batch_host_ctx"}
     del host
 
     # ---- cfg5 (BASELINE configs[4]): 2^23 points sharded over the ranks, compute-only and
@@ -374,8 +374,7 @@ def main(argv=None):
             ref, sabs = oracle.hvp_batch(args.func, synth.points(0, n, CFG5_M_TOTAL)[chk],
                                          synth.vectors(0, n, CFG5_M_TOTAL)[chk], C, params_np[args.func])
             ok = bool(oracle.componentwise_error(res[chk].cpu().numpy(), ref, sabs).max() <= 1e-10)
-        strong = {"workload": f"cfg5: {args.func} n={n} C={C} m={CFG5_M_TOTAL} over {world} GPU(s)",
-                  "value": CFG5_M_TOTAL / tc, "ms": tc * 1e3, "value_with_gather": CFG5_M_TOTAL / tg,
+        strong = {"workload": f"cfg5 m={CFG5_M_TOTAL}", "value": CFG5_M_TOTAL / tc, "ms": tc * 1e3, "value_with_gather": CFG5_M_TOTAL / tg,
                   "ms_with_gather": tg * 1e3, "gather": gb.kind, "gather_parity": ok}
         del gb, p5, v5, o5, res
 
@@ -384,6 +383,11 @@ def main(argv=None):
     if not args.no_sweep and world == 1:
         sweep, paper_l2 = run_sweep(chf, args, pts, vec, out, params, stream, m, m_all, peak_tf, per_step,
                                     timed_steps, max_over_ranks)
+
+    # ---- n = 2 / 4 at m = 2^24 (inputs >> L2): the HBM-bound corner of §8(d)
+    small_hbm = []
+    if not args.no_sweep and world == 1:
+        small_hbm = run_small_n_hbm(chf, dev, stream, timed_steps, float(peaks.get("hbm_gbs", 0.0)) or None)
 
     # ---- CPU baseline: the oracle on the host cores, rank 0 at N=1 only
     cpu = None
@@ -411,33 +415,36 @@ def main(argv=None):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per_step * 1e3,
-            "step_ms": {"median": step_med * 1e3, "best": step_best * 1e3, "samples": args.steps},
+            "step_ms": {"median": step_med * 1e3, "best": step_best * 1e3},
             "higher_is_better": True, "scaling": "strong" if args.m_total else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_config(args, world),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf,
                          "frac_executed": None if exec_tf is None else exec_tf / peak_tf,
-                         "frac_model": model_tf / peak_tf, "achieved_model": model_tf,
+                         "frac_model": model_tf / peak_tf,
                          "executed_over_model": None if ex is None else ex["executed_flops_per_point"] / flops_pt,
                          "model_flops_per_point": flops_pt, "traffic": traffic, "algorithmic_bytes": alg_bytes,
                          "hbm_gbs": alg_bytes / per_step / 1e9,
                          "fp64_pipe_pct_ncu": None if ex is None else ex["fp64_pipe_active_pct"],
-                         "basis": ("frac = executed FP64 FLOPs (ncu 2*DFMA+DMUL+DADD, " +
-                                   (ex["basis"] if ex else "missing") + ") / derived peak; frac_model = §8(d) "
-                                   "model FLOPs (nvcc folds 0/1 seed products, so model > executed)"),
-                         "peak_basis": f"derived {SMS} SM x {FP64_FMA_PER_SM_CLK} FMA/clk x 2 x {peak_mhz:.0f} MHz",
+                         "basis": "frac: ncu-executed 2*DFMA+DMUL+DADD (" + (
+                             ("SASS " + ex["sass_hash"]) if ex and ex.get("sass_hash") else "n/a") +
+                             "); frac_model: §8(d) model (DESIGN.md §5)",
+                         "peak_basis": f"{SMS}x{FP64_FMA_PER_SM_CLK}x2x{peak_mhz:.0f}MHz",
                          "fp64_probe_tflops": probe_tf},
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": args.steps, "clocks": clocks, "parity": parity, "strong": strong,
             "sweep_best_hvp": sweep_best,
+            "small_n_hbm_frac": {f"{r['func'][:4]} n={r['n']}": r["hbm_frac"] for r in small_hbm
+                                 if r.get("best") and r["func"] != "ackley"},
             "paper_l2_speedup": None if paper_l2 is None else paper_l2["ours_over_paper_l2"],
             "sweep_file": os.path.relpath(args.sweep_out, ROOT) if sweep else None,
         }
         if sweep:
             os.makedirs(os.path.dirname(args.sweep_out), exist_ok=True)
             with open(args.sweep_out, "w") as f:
-                json.dump({"headline": line, "sweep": sweep, "paper_l2_baseline": paper_l2}, f, indent=1)
-        print(json.dumps(line, separators=(",", ":")), flush=True)
+                json.dump({"headline": line, "sweep": sweep, "paper_l2_baseline": paper_l2, "small_n_hbm": small_hbm},
+                          f, indent=1)
+        print(json.dumps(_round(line), separators=(",", ":")), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -487,6 +494,35 @@ def run_sweep(chf, args, pts, vec, out, params, stream, m, m_all, peak_tf, per_s
     return sweep, paper_l2
 
 
+def run_small_n_hbm(chf, dev, stream, timed_steps, hbm_peak):
+    """chessfad_hvp_batch at n = 2 and 4 over m = 2^24 points (1.6 GB of traffic at n = 4,
+    far beyond the 126 MB L2): algorithmic bytes 24n per point / event time vs measured HBM."""
+    import torch
+    m = 1 << 24
+    rows = []
+    for n in (2, 4):
+        pts = torch.from_numpy(synth.points(0, n, m)).to(dev)
+        vec = torch.from_numpy(synth.vectors(0, n, m)).to(dev)
+        out = torch.empty_like(pts)
+        for f in ("rosenbrock", "ackley", "prodsum"):
+            best = None
+            for c in (1, 2, 4):
+                if n % c or not chf.is_supported(f, n, c):
+                    continue
+                tt, per = timed_steps(lambda: chf.hvp_batch(f, pts, vec, c, None, out=out), 10, 3)
+                tt /= 10
+                gbs = 24 * n * m / tt / 1e9
+                r = {"func": f, "n": n, "csize": c, "m": m, "ms": tt * 1e3, "ms_median": float(np.median(per)) * 1e3,
+                     "hvp_per_s": m / tt, "hbm_gbs": gbs, "hbm_frac": gbs / hbm_peak if hbm_peak else None}
+                rows.append(r)
+                if best is None or tt < best["ms"] / 1e3:
+                    best = r
+            if best is not None:
+                best["best"] = True
+        del pts, vec, out
+    return rows
+
+
 def executed_entry(func, n, C, src_hash, algo="hvp", path=None):
     """ncu-measured executed FLOPs/point of this build (profiles/executed_flops.json).  If the
     table was measured on an earlier build, its executed/model ratio is applied to this build's
@@ -512,6 +548,17 @@ def executed_entry(func, n, C, src_hash, algo="hvp", path=None):
         ent["executed_flops_per_point"] = ratio * chf.model_flops_per_point(func, n, C, algo=algo)
         ent["basis"] = f"STALE: executed/model ratio {ratio:.3f} measured by ncu on build {tab.get('src_hash')}"
     return ent
+
+
+def _round(x):
+    """4 significant digits for the printed line (the sweep file keeps full precision)."""
+    if isinstance(x, float):
+        return float(f"{x:.4g}")
+    if isinstance(x, dict):
+        return {k: _round(v) for k, v in x.items()}
+    if isinstance(x, list):
+        return [_round(v) for v in x]
+    return x
 
 
 class _Null:
