@@ -156,14 +156,38 @@ cudaError_t dispatch_small(int C, const BatchArgs& a, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
+#ifndef CHF_STREAM_SMALL
+#define CHF_STREAM_SMALL 1  // Alg 7 at n in {2, 4, 8} through hvp_stream_kernel (0: runtime-n kernel)
+#endif
+template <int F>
+cudaError_t dispatch_stream(int C, const BatchArgs& a, cudaStream_t s) {
+#define CHF_STREAM_CASE(FF, CC, NS) \
+  if (C == CC && a.n == NS) return launch_stream<FF, CC, NS>(a, s);
+  CHF_FOR_STREAM(CHF_STREAM_CASE, F)
+#undef CHF_STREAM_CASE
+  return cudaErrorInvalidValue;
+}
+
+bool aligned16(const BatchArgs& a) {
+  return ((reinterpret_cast<uintptr_t>(a.points) | reinterpret_cast<uintptr_t>(a.vecs) |
+           reinterpret_cast<uintptr_t>(a.out)) & 15) == 0;
+}
+
 template <int MODE>
 cudaError_t dispatch_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s) {
   const int C = reg_kernel_chunk(Capi);
+  if constexpr (MODE == MODE_HVP) {
+    if (CHF_STREAM_SMALL && (a.n == 2 || a.n == 4 || a.n == 8) && aligned16(a)) {
+      switch (func) {
+        case CHESSFAD_ROSENBROCK: return dispatch_stream<FUNC_ROSENBROCK>(C, a, s);
+        case CHESSFAD_ACKLEY: return dispatch_stream<FUNC_ACKLEY>(C, a, s);
+        case CHESSFAD_PRODSUM: return dispatch_stream<FUNC_PRODSUM>(C, a, s);
+      }
+    }
+  }
   if constexpr (MODE == MODE_HVP_ROWHOIST) {  // NEXT-4 (chessfad_hvp_batch_hoisted), register path
     // the compile-time kernels use 16-byte double2 loads/stores of whole point rows
-    const bool aligned = ((reinterpret_cast<uintptr_t>(a.points) | reinterpret_cast<uintptr_t>(a.vecs) |
-                           reinterpret_cast<uintptr_t>(a.out)) & 15) == 0;
-    if (aligned && (a.n == 2 || a.n == 4 || a.n == 8 || a.n == 16)) {
+    if (aligned16(a) && (a.n == 2 || a.n == 4 || a.n == 8 || a.n == 16)) {
       switch (func) {
         case CHESSFAD_ROSENBROCK: return dispatch_small<FUNC_ROSENBROCK>(C, a, s);
         case CHESSFAD_ACKLEY: return dispatch_small<FUNC_ACKLEY>(C, a, s);

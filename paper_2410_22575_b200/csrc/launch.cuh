@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include "f3_sparse.cuh"  // includes kernels.cuh
+#include "stream_small.cuh"
 
 namespace chessfad {
 
@@ -140,6 +141,35 @@ cudaError_t launch_small(BatchArgs a, cudaStream_t s) {
 CHF_FOR_SMALL(CHF_DECL_SMALL, FUNC_ROSENBROCK)
 CHF_FOR_SMALL(CHF_DECL_SMALL, FUNC_ACKLEY)
 CHF_FOR_SMALL(CHF_DECL_SMALL, FUNC_PRODSUM)
+
+// Alg 7 at n = NS in {2, 4, 8}: thread per point, persistent grid, bulk-copy ring
+// (stream_small.cuh).  Grid = min(tiles, SMs x resident CTAs), resident CTAs queried once.
+template <int FUNC, int C, int NS>
+cudaError_t launch_stream(BatchArgs a, cudaStream_t s) {
+  auto kern = hvp_stream_kernel<BuiltinFunc<FUNC>, C, NS>;
+  constexpr size_t smem = StreamCfg<NS>::kSmem;
+  static int occ = 0;
+  cudaError_t e;
+  if (occ == 0) {
+    if (smem > 48 * 1024 &&
+        (e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+      return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kStreamTP, smem)) != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+  }
+  int dev = 0, sms = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  const int64_t tiles = (a.m + kStreamTP - 1) / kStreamTP;
+  const int grid = (int)(tiles < (int64_t)sms * occ ? tiles : (int64_t)sms * occ);
+  kern<<<grid, kStreamTP, smem, s>>>(a, BuiltinFunc<FUNC>{});
+  return cudaGetLastError();
+}
+#define CHF_FOR_STREAM(X, F) X(F, 1, 2) X(F, 2, 2) X(F, 1, 4) X(F, 2, 4) X(F, 4, 4) X(F, 1, 8) X(F, 2, 8) X(F, 4, 8) X(F, 8, 8)
+#define CHF_DECL_STREAM(F, C, NS) extern template cudaError_t launch_stream<F, C, NS>(BatchArgs, cudaStream_t);
+CHF_FOR_STREAM(CHF_DECL_STREAM, FUNC_ROSENBROCK)
+CHF_FOR_STREAM(CHF_DECL_STREAM, FUNC_ACKLEY)
+CHF_FOR_STREAM(CHF_DECL_STREAM, FUNC_PRODSUM)
 
 // explicit-instantiation declarations (definitions in inst_*.cu)
 #define CHF_FOR_MODE(X, A, B) \

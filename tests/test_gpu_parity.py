@@ -234,6 +234,29 @@ def test_cfg2_every_point(chf, func):
             assert cfn.error(got, hv, S) <= TIGHT, (algo, C)
 
 
+# ------------------------------------------------------------ n in {2, 4, 8}: the bulk-copy streaming kernel
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_stream_small_persistent(chf, n):
+    """hvp_stream_kernel (stream_small.cuh): enough tiles that every CTA of the persistent
+    grid cycles its shared-memory ring several times, a ragged last tile, every point checked;
+    a 16-byte-misaligned view takes the runtime-n kernel and agrees."""
+    m = {2: 1_500_007, 4: 600_011, 8: 150_001}[n]
+    P, V = synth.points(30, n, m), synth.vectors(30, n, m)
+    dev = torch.device("cuda")
+    for func in ("rosenbrock", "ackley", "prodsum"):
+        ref, sabs = oracle.hvp_batch(func, P, V, 1, None)
+        for C in divisors(n):
+            _check(_gpu_hvp(chf, func, P, V, C), ref, sabs)
+        k = min(m, 4099)
+        flat_p = torch.empty(k * n + 1, dtype=torch.float64, device=dev)
+        flat_v = torch.empty(k * n + 1, dtype=torch.float64, device=dev)
+        flat_o = torch.empty(k * n + 1, dtype=torch.float64, device=dev)
+        flat_p[1:] = torch.from_numpy(P[:k].ravel()).to(dev)
+        flat_v[1:] = torch.from_numpy(V[:k].ravel()).to(dev)
+        got = chf.hvp_batch(func, flat_p[1:].view(k, n), flat_v[1:].view(k, n), 1, out=flat_o[1:].view(k, n))
+        _check(got.cpu().numpy(), ref[:k], sabs[:k])
+
+
 # ------------------------------------------------------------ NEXT-1 / NEXT-2: symmetric algorithms
 @pytest.mark.parametrize("func", FUNCS)
 @pytest.mark.parametrize("n", [2, 6, 16, 32])
