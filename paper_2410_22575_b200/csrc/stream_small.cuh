@@ -153,6 +153,11 @@ __global__ void __launch_bounds__(kStreamTP, NS == 8 ? 1 : 2) hvp_stream_kernel(
         v[2 * q + 1] = w.y;
       }
     }
+    // WAR across proxies: the refill below is an async-proxy (TMA) write, which bar.sync alone
+    // does not order after these generic-proxy shared loads (they may still be queued --
+    // measured: whole warps read the NEXT tile at n = 8).  Each thread's proxy fence orders
+    // its loads before the barrier, the barrier before the refill.
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();  // every thread holds its point: stage s may be refilled
     if (tid == 0) {
       const int64_t nxt = tile + (int64_t)S * gridDim.x;
