@@ -248,6 +248,15 @@ double chessfad_model_flops_per_point_algo(int func, int n, int csize, int algo)
  */
 int chessfad_fp64_probe(int blocks, int64_t iters, double *sink, void *stream);
 
+/*
+ * Which kernel family a call with these arguments runs (introspection for tests and the bench;
+ * DESIGN.md §3 describes each): "reg" (hDual<C> in registers, lane = point, warp = row),
+ * "stream" (n in {2,4,8}, thread per point, bulk-copy ring; 16-byte-aligned buffers, else
+ * "reg"), "small_hoisted", "reg_seedsparse", "f3_dmma" (Fletcher-Powell E-sums on the FP64
+ * tensor core), "f3_simt", "f3_seedsparse", or "unsupported".  Static string, never NULL.
+ */
+const char *chessfad_path(int func, int n, int csize, int algo);
+
 /* Library version string. */
 const char *chessfad_version(void);
 

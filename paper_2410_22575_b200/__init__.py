@@ -26,7 +26,7 @@ EXPORTS = sorted(["chessfad_hvp_batch", "chessfad_hessian_batch", "chessfad_sym_
                   "chessfad_fp64_probe", "chessfad_version", "chessfad_hvp_host_workspace_bytes",
                   "chessfad_hvp_batch_hoisted", "chessfad_hvp_batch_seedsparse", "chessfad_hessian_batch_seedsparse", "chessfad_hvp_batch_paper_l2", "chessfad_hessian_grad_batch",
                   "chessfad_hvp_batch_paper", "chessfad_host_ctx_create", "chessfad_host_ctx_destroy",
-                  "chessfad_hvp_batch_host_ctx"])
+                  "chessfad_hvp_batch_host_ctx", "chessfad_path"])
 
 _lock = threading.Lock()
 _lib = None
@@ -75,6 +75,7 @@ def load(build_if_missing: bool = True):
             "chessfad_model_flops_per_point": (dbl, [i32, i32, i32, i32]),
             "chessfad_fp64_probe": (i32, [i32, i64, vp, vp]),
             "chessfad_version": (ctypes.c_char_p, []),
+            "chessfad_path": (ctypes.c_char_p, [i32, i32, i32, i32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -333,6 +334,11 @@ def model_flops_per_point(func, n: int, csize: int, hessian: bool = False, algo:
 
 def fp64_probe(blocks: int, iters: int, sink, stream=None):
     _check(load().chessfad_fp64_probe(blocks, iters, _dev(sink, "sink"), _stream_ptr(stream)))
+
+
+def path(func, n: int, csize: int, algo: str = "hvp") -> str:
+    """Kernel family that runs for these arguments (chessfad_path): e.g. "f3_dmma", "stream"."""
+    return load().chessfad_path(_func(func), n, csize, ALGOS[algo]).decode()
 
 
 def version() -> str:

@@ -58,9 +58,16 @@ int validate(int func, int n, int csize, int64_t m, bool need_params_ptr, const 
 
 constexpr size_t kSmemMax = 227 * 1024;
 
+#ifndef CHF_F3_MMA
+#define CHF_F3_MMA 1  // F3 at n in {8, 16, ..., 64} on the FP64 tensor core (0: SIMT slot-column kernel)
+#endif
+bool f3_mma_n(int n) { return CHF_F3_MMA && n % 8 == 0 && n >= 8 && n <= 64; }
+
 int supported(int func, int n, int csize, int mode) {
   (void)csize;  // every C | n runs (F3: runtime C; register path: reg_kernel_chunk)
   if (mode == MODE_HVP_ROWHOIST) mode = MODE_HVP;  // same shapes as the per-evaluation HVP
+  if (func == CHESSFAD_FLETCHER_POWELL && f3_mma_n(n))  // tensor-core kernel: every mode
+    return F3MmaCfg<64>::smem_bytes(true) <= kSmemMax;
   if (func == CHESSFAD_FLETCHER_POWELL)  // n > 32 streams (A, B) in 8-column cp.async stages
     return n <= kMaxNF3 && (n <= 32 || n % kF3RingJ == 0) &&
            f3_smem_bytes(n, groups_for(n, kWarpsF3, mode), mode) <= kSmemMax;
@@ -168,6 +175,13 @@ cudaError_t dispatch_stream(int C, const BatchArgs& a, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
+// the stream kernel is used where it measured faster than the runtime-n kernel at m = 2^24
+// (profiles/r02/d/ab: 1.5-6x, except Ackley n = 8 with C <= 2: 1.2-1.4x slower, register-bound)
+bool stream_small_n(int func, int n, int C) {
+  if (!CHF_STREAM_SMALL || !(n == 2 || n == 4 || n == 8)) return false;
+  return !(func == CHESSFAD_ACKLEY && n == 8 && C <= 2);
+}
+
 bool aligned16(const BatchArgs& a) {
   return ((reinterpret_cast<uintptr_t>(a.points) | reinterpret_cast<uintptr_t>(a.vecs) |
            reinterpret_cast<uintptr_t>(a.out)) & 15) == 0;
@@ -177,7 +191,7 @@ template <int MODE>
 cudaError_t dispatch_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s) {
   const int C = reg_kernel_chunk(Capi);
   if constexpr (MODE == MODE_HVP) {
-    if (CHF_STREAM_SMALL && (a.n == 2 || a.n == 4 || a.n == 8) && aligned16(a)) {
+    if (stream_small_n(func, a.n, C) && aligned16(a)) {
       switch (func) {
         case CHESSFAD_ROSENBROCK: return dispatch_stream<FUNC_ROSENBROCK>(C, a, s);
         case CHESSFAD_ACKLEY: return dispatch_stream<FUNC_ACKLEY>(C, a, s);
@@ -217,6 +231,14 @@ cudaError_t dispatch_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s)
 
 template <int MODE>
 cudaError_t dispatch_f3(const BatchArgs& a, cudaStream_t s) {
+  if (f3_mma_n(a.n)) {
+    switch (a.n) {
+#define CHF_MMA_CASE(NN) \
+  case NN: return launch_f3_mma<NN, MODE>(a, s);
+      CHF_FOR_MMA_NN(CHF_MMA_CASE)
+#undef CHF_MMA_CASE
+    }
+  }
   const bool ab_smem = f3_ab_smem(a.n);
 #define CHF_CASE_KB(KB) \
   case KB: return ab_smem ? launch_f3<KB, MODE, true>(a, s) : launch_f3<KB, MODE, false>(a, s);
@@ -535,6 +557,20 @@ int chessfad_fp64_probe(int blocks, int64_t iters, double* sink, void* stream) {
   if (blocks < 1 || iters < 0 || !sink) return CHESSFAD_ERR_ARG;
   fp64_probe_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(iters, sink);
   return cudaGetLastError() == cudaSuccess ? CHESSFAD_OK : CHESSFAD_ERR_CUDA;
+}
+
+const char* chessfad_path(int func, int n, int csize, int algo) {
+  if (!chessfad_is_supported_algo(func, n, csize, algo)) return "unsupported";
+  const bool sparse = algo == CHESSFAD_ALGO_HVP_SEEDSPARSE || algo == CHESSFAD_ALGO_HESSIAN_SEEDSPARSE;
+  if (func == CHESSFAD_FLETCHER_POWELL) {
+    if (sparse) return "f3_seedsparse";
+    return f3_mma_n(n) ? "f3_dmma" : "f3_simt";
+  }
+  if (sparse) return "reg_seedsparse";
+  const int C = reg_kernel_chunk(csize);
+  if (algo == CHESSFAD_ALGO_HVP && stream_small_n(func, n, C)) return "stream";  // 16-byte-aligned buffers
+  if (algo == CHESSFAD_ALGO_HVP_HOISTED && (n == 2 || n == 4 || n == 8 || n == 16)) return "small_hoisted";
+  return "reg";
 }
 
 const char* chessfad_version(void) { return "chessfad-b200 0.1.0 (sm_100a)"; }

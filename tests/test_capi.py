@@ -194,3 +194,18 @@ def test_hessian_grad_contract(lib):
     vp = ctypes.c_void_p
     # grad NULL with m > 0 -> ERR_ARG, before any CUDA call
     assert lib.chessfad_hessian_grad_batch(0, 16, 4, 10, vp(1), vp(1), None, None, None) == 1
+
+
+def test_kernel_path_introspection():
+    """chessfad_path names the kernel family each call runs."""
+    import paper_2410_22575_b200 as chf
+    assert chf.path("fletcher_powell", 16, 4) == "f3_dmma"
+    assert chf.path("fletcher_powell", 64, 8, "sym_hvp") == "f3_dmma"
+    assert chf.path("fletcher_powell", 128, 8) == "f3_simt"
+    assert chf.path("fletcher_powell", 12, 4) == "f3_simt"
+    assert chf.path("fletcher_powell", 16, 4, "hvp_seedsparse") == "f3_seedsparse"
+    assert chf.path("rosenbrock", 2, 1) == "stream"
+    assert chf.path("rosenbrock", 16, 16) == "reg"
+    assert chf.path("ackley", 8, 1) == "reg" and chf.path("ackley", 8, 4) == "stream"
+    assert chf.path("rosenbrock", 8, 2, "hvp_hoisted") == "small_hoisted"
+    assert chf.path("rosenbrock", 3, 2) == "unsupported"

@@ -349,8 +349,19 @@ def test_seedsparse_f3(chf, n, m):
         b = chf.hvp_batch_seedsparse("fletcher_powell", p, v, C, pr).cpu().numpy()
         if (n <= 64 or C == n) and chf.is_supported("fletcher_powell", n, C, "hvp"):
             a = chf.hvp_batch("fletcher_powell", p, v, C, pr).cpu().numpy()
-            assert np.array_equal(a, b), f"C={C}: max |diff| {np.abs(a - b).max():.3e}"
+            _same_as_per_eval(chf, n, C, a, b)
         _check(b[:ms], ref, sabs)
+
+
+def _same_as_per_eval(chf, n, C, a, b, algo="hvp"):
+    """Seed-sparse vs the per-evaluation path: bit for bit (up to the sign of zero) against
+    the SIMT slot-column kernel, whose operation order it copies; within rounding of the
+    tensor-core kernel (DMMA sums the 4 terms of each k-step in its own order)."""
+    if chf.path("fletcher_powell", n, C, algo) == "f3_simt":
+        assert np.array_equal(a, b), f"C={C}: max |diff| {np.abs(a - b).max():.3e}"
+    else:
+        scale = np.abs(a).max(axis=tuple(range(1, a.ndim)), keepdims=True)
+        assert (np.abs(a - b) / scale).max() <= TIGHT, f"C={C}: max rel diff {(np.abs(a - b) / scale).max():.3e}"
 
 
 @pytest.mark.parametrize("n,m", [(2, 100), (8, 70), (32, 50), (64, 9), (128, 5)])
@@ -365,7 +376,7 @@ def test_seedsparse_f3_hessian(chf, n, m):
     for C in sorted({1, n}):
         a = chf.hessian_batch("fletcher_powell", p, C, pr).cpu().numpy()
         b = chf.hessian_batch_seedsparse("fletcher_powell", p, C, pr).cpu().numpy()
-        assert np.array_equal(a, b)
+        _same_as_per_eval(chf, n, C, a, b, algo="hessian")
         rel = np.max(np.abs(b - Href), axis=(1, 2)) / np.max(np.abs(Href), axis=(1, 2))
         assert rel.max() <= TIGHT
 
@@ -383,7 +394,10 @@ def test_seedsparse_register_functions(chf, func, n, m):
     for C in sorted({1, n if n <= 32 else 32} | ({2} if n % 2 == 0 else set())):
         a = chf.hvp_batch(func, p, v, C).cpu().numpy()
         b = chf.hvp_batch_seedsparse(func, p, v, C).cpu().numpy()
-        assert np.array_equal(a, b), f"C={C}: max |diff| {np.abs(a - b).max():.3e}"
+        if chf.path(func, n, C) == "stream":  # the register-resident kernel: its own FMA contraction
+            _check(a, ref, sabs)
+        else:
+            assert np.array_equal(a, b), f"C={C}: max |diff| {np.abs(a - b).max():.3e}"
         _check(b, ref, sabs)
         if n <= 64:
             Ha = chf.hessian_batch(func, p[:16], C).cpu().numpy()
