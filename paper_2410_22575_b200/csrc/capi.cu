@@ -61,13 +61,16 @@ constexpr size_t kSmemMax = 227 * 1024;
 #ifndef CHF_F3_MMA
 #define CHF_F3_MMA 1  // F3 at n in {8, 16, ..., 64} on the FP64 tensor core (0: SIMT slot-column kernel)
 #endif
-bool f3_mma_n(int n) { return CHF_F3_MMA && n % 8 == 0 && n >= 8 && n <= 64; }
+#ifndef CHF_F3_MMA_MINN
+#define CHF_F3_MMA_MINN 5  // smaller n: the SIMT kernel (padding to 8 would multiply the E-sum work)
+#endif
+bool f3_mma_n(int n) { return CHF_F3_MMA && n >= CHF_F3_MMA_MINN && n <= 128; }
 
 int supported(int func, int n, int csize, int mode) {
   (void)csize;  // every C | n runs (F3: runtime C; register path: reg_kernel_chunk)
   if (mode == MODE_HVP_ROWHOIST) mode = MODE_HVP;  // same shapes as the per-evaluation HVP
   if (func == CHESSFAD_FLETCHER_POWELL && f3_mma_n(n))  // tensor-core kernel: every mode
-    return F3MmaCfg<64>::smem_bytes(true) <= kSmemMax;
+    return F3Mma<64, MODE_SYM_HVP>::smem_bytes() <= kSmemMax && F3Mma<128, MODE_SYM_HVP>::smem_bytes() <= kSmemMax;
   if (func == CHESSFAD_FLETCHER_POWELL)  // n > 32 streams (A, B) in 8-column cp.async stages
     return n <= kMaxNF3 && (n <= 32 || n % kF3RingJ == 0) &&
            f3_smem_bytes(n, groups_for(n, kWarpsF3, mode), mode) <= kSmemMax;
@@ -232,7 +235,7 @@ cudaError_t dispatch_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s)
 template <int MODE>
 cudaError_t dispatch_f3(const BatchArgs& a, cudaStream_t s) {
   if (f3_mma_n(a.n)) {
-    switch (a.n) {
+    switch ((a.n + 7) / 8 * 8) {
 #define CHF_MMA_CASE(NN) \
   case NN: return launch_f3_mma<NN, MODE>(a, s);
       CHF_FOR_MMA_NN(CHF_MMA_CASE)

@@ -1,4 +1,4 @@
-// inst_f3mma_48.cu -- F3 tensor-core kernels (hvp_f3_mma_kernel, f3_mma.cuh) for n = 48, all modes.
+// inst_f3mma_48.cu -- F3 tensor-core kernels (hvp_f3_mma_kernel, f3_mma.cuh) for n <= 48, all modes.
 #include "launch.cuh"
 
 namespace chessfad {

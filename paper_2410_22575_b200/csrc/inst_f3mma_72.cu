@@ -1,7 +1,7 @@
-// inst_f3mma_40.cu -- F3 tensor-core kernels (hvp_f3_mma_kernel, f3_mma.cuh) for n <= 40, all modes.
+// inst_f3mma_72.cu -- F3 tensor-core kernels (hvp_f3_mma_kernel, f3_mma.cuh) for n <= 72, all modes.
 #include "launch.cuh"
 
 namespace chessfad {
 #define CHF_INST_MMA1(NN, M) template cudaError_t launch_f3_mma<NN, M>(BatchArgs, cudaStream_t);
-CHF_FOR_MMA_MODE(CHF_INST_MMA1, 40)
+CHF_FOR_MMA_MODE(CHF_INST_MMA1, 72)
 }  // namespace chessfad

@@ -172,16 +172,17 @@ CHF_FOR_STREAM(CHF_DECL_STREAM, FUNC_ROSENBROCK)
 CHF_FOR_STREAM(CHF_DECL_STREAM, FUNC_ACKLEY)
 CHF_FOR_STREAM(CHF_DECL_STREAM, FUNC_PRODSUM)
 
-// F3 with the E-sums on the FP64 tensor core (f3_mma.cuh), n = NN compile-time
+// F3 with the E-sums on the FP64 tensor core (f3_mma.cuh): n <= NN (zero-padded), NN = 8 ceil(n / 8)
 template <int NN, int MODE>
 cudaError_t launch_f3_mma(BatchArgs a, cudaStream_t s) {
-  const size_t smem = F3MmaCfg<NN>::smem_bytes(MODE == MODE_SYM_HVP);
-  const int grid = (int)((a.m + kMmaP - 1) / kMmaP);
-  return launch_with_smem(hvp_f3_mma_kernel<NN, MODE>, grid, kMmaWarps * 32, smem, s, a);
+  using Cfg = F3Mma<NN, MODE>;
+  const int grid = (int)((a.m + Cfg::P - 1) / Cfg::P);
+  return launch_with_smem(hvp_f3_mma_kernel<NN, MODE>, grid, Cfg::W * 32, Cfg::smem_bytes(), s, a);
 }
 #define CHF_FOR_MMA_MODE(X, NN) X(NN, MODE_HVP) X(NN, MODE_HESS) X(NN, MODE_SYM_HVP) X(NN, MODE_SYM_HESS) \
   X(NN, MODE_HESS_GRAD) X(NN, MODE_HVP_ROWHOIST)
-#define CHF_FOR_MMA_NN(X) X(8) X(16) X(24) X(32) X(40) X(48) X(56) X(64)
+#define CHF_FOR_MMA_NN(X) X(8) X(16) X(24) X(32) X(40) X(48) X(56) X(64) X(72) X(80) X(88) X(96) X(104) X(112) \
+  X(120) X(128)
 #define CHF_DECL_MMA1(NN, M) extern template cudaError_t launch_f3_mma<NN, M>(BatchArgs, cudaStream_t);
 #define CHF_DECL_MMA(NN) CHF_FOR_MMA_MODE(CHF_DECL_MMA1, NN)
 CHF_FOR_MMA_NN(CHF_DECL_MMA)

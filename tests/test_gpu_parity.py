@@ -278,6 +278,39 @@ def test_sym_hvp_parity(chf, func, n):
         _check(got, ref7, sabs)
 
 
+@pytest.mark.parametrize("n,m", [(12, 77), (20, 65), (64, 41), (72, 19), (100, 9), (128, 9)])
+def test_f3_dmma_all_modes(chf, n, m):
+    """Fletcher-Powell on the tensor-core kernel (f3_mma.cuh): zero-padded n (12, 20, 72, 100),
+    the k-blocked M (n > 64) and a ragged CTA, every entry point -- Alg 7, Alg 8 (now for every
+    n <= 128), Alg 5, Alg 6, gradient, row-hoisted -- against the oracle (the closed form for
+    the Hessian at the sampled points)."""
+    func = "fletcher_powell"
+    P, V = synth.points(40, n, m), synth.vectors(40, n, m)
+    params = _params(func, n)
+    dev = torch.device("cuda")
+    p, v, pr = (torch.from_numpy(x).to(dev) for x in (P, V, params))
+    ms = m if n <= 72 else 4  # oracle cost at n = 128: ~3 s per point and C
+    ref, sabs = oracle.hvp_batch(func, P[:ms], V[:ms], n, params)
+    Cs = sorted({1, 4 if n % 4 == 0 else 1, n // 2 if n % 2 == 0 else n, n})
+    hs = [0, m - 1] if n > 72 else list(range(m))
+    Href = np.stack([cf.to_float(cf.fp_hessian_mp(P[e], params[:n * n].reshape(n, n),
+                                                   params[n * n:2 * n * n].reshape(n, n), params[2 * n * n:]))
+                     for e in hs]) if n <= 20 else oracle.hessian_batch(func, P[hs], n, params)
+    for C in Cs:
+        assert chf.path(func, n, C) == "f3_dmma"
+        for entry in ("hvp_batch", "sym_hvp_batch", "hvp_batch_hoisted"):
+            got = getattr(chf, entry)(func, p, v, C, pr).cpu().numpy()
+            _check(got[:ms], ref, sabs)
+        for entry in ("hessian_batch", "sym_hessian_batch"):
+            H = getattr(chf, entry)(func, p, C, pr).cpu().numpy()[hs]
+            rel = np.abs(H - Href).max(axis=(1, 2)) / np.abs(Href).max(axis=(1, 2))
+            assert rel.max() <= TIGHT, (entry, C, rel.max())
+        Hg, grad = chf.hessian_grad_batch(func, p, C, pr)
+        g_ref = np.stack([oracle.hessian(func, P[e], params, algo="chunk", C=n)[1] for e in hs[:2]])
+        gs = np.abs(g_ref).max(axis=1, keepdims=True)
+        assert (np.abs(grad.cpu().numpy()[hs[:2]] - g_ref) / gs).max() <= TIGHT
+
+
 @pytest.mark.parametrize("func", ["rosenbrock", "prodsum"])
 def test_sym_hvp_integer_bitwise(chf, func):
     n, m = 16, 200

@@ -26,12 +26,15 @@ def load(csv_path, order_path):
         algo = order[lid][6].split("=")[1] if len(order[lid]) > 6 else "hvp"
         n, C, m = int(n[2:]), int(C[2:]), int(m[2:])
         model = float(fl.split("=")[1]) * m
-        ex = 2 * v["sm__sass_thread_inst_executed_op_dfma_pred_on.sum"] + v["sm__sass_thread_inst_executed_op_dmul_pred_on.sum"] + v["sm__sass_thread_inst_executed_op_dadd_pred_on.sum"]
+        dmma = v.get("sm__inst_executed_pipe_tensor_subpipe_dmma.sum", 0.0)  # m8n8k4: 256 FMAs per warp instruction
+        ex = 2 * v["sm__sass_thread_inst_executed_op_dfma_pred_on.sum"] + v["sm__sass_thread_inst_executed_op_dmul_pred_on.sum"] + v["sm__sass_thread_inst_executed_op_dadd_pred_on.sum"] + 512 * dmma
         t = v["gpu__time_duration.sum"] * 1e-9
         out.append({"func": func, "n": n, "C": C, "m": m, "algo": algo, "kernel": v["__kernel"], "time_ms": t * 1e3,
                     "model_flops": model, "executed_flops": ex, "executed_over_model": ex / model,
                     "fp64_warp_inst": v["sm__inst_executed_pipe_fp64.sum"],
                     "fp64_pipe_active_pct": v["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"],
+                    "dmma_warp_inst": dmma,
+                    "dmma_pipe_active_pct": v.get("smsp__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active"),
                     "executed_flop_per_fp64_lane_inst": ex / (32 * v["sm__inst_executed_pipe_fp64.sum"]),
                     "all_warp_inst": v["smsp__inst_executed.sum"],
                     "fp64_inst_share": v["sm__inst_executed_pipe_fp64.sum"] / v["smsp__inst_executed.sum"],
@@ -64,12 +67,15 @@ def update_table(res, table_path):
         tab["entries"][key] = {"executed_flops_per_point": r["executed_flops"] / r["m"],
                                "model_flops_per_point": r["model_flops"] / r["m"],
                                "fp64_pipe_active_pct": r["fp64_pipe_active_pct"],
+                               "dmma_pipe_active_pct": r.get("dmma_pipe_active_pct"),
+                               "dmma_flops_per_point": 512 * r.get("dmma_warp_inst", 0.0) / r["m"],
                                "dram_bytes_per_launch": r["dram_bytes"], "m": r["m"], "regs": r["regs"],
                                "ncu_time_ms": r["time_ms"], "kernel": r["kernel"],
                                "sass_hash": sass_hash_for(LIB_PATH, r["kernel"])}
     tab["note"] = ("entries are valid for the kernel SASS whose sha256 is sass_hash (paper_2410_22575_b200/sass.py); "
                    "executed FP64 FLOPs = 2*DFMA + DMUL + DADD thread instructions (ncu "
-                   "sm__sass_thread_inst_executed_op_{dfma,dmul,dadd}_pred_on.sum) per point, one launch each; "
+                   "sm__sass_thread_inst_executed_op_{dfma,dmul,dadd}_pred_on.sum) + 512 per DMMA m8n8k4 warp "
+                   "instruction (sm__inst_executed_pipe_tensor_subpipe_dmma.sum) per point, one launch each; "
                    "tools/profile_sweep.py under ncu, summarised by tools/summarize_sweep.py")
     json.dump(tab, open(table_path, "w"), indent=1, sort_keys=True)
 
