@@ -16,12 +16,15 @@
 //     writes its n results with 16-byte coalesced stores.
 //
 // Per-evaluation execution.  The row / chunk / variable loops are unrolled (NS is a
-// compile-time constant, so the point, vector and result live in registers), but the row
-// index, the chunk start and the point's coordinates are passed to every evaluation through
-// opaque register moves (opq): to the compiler they are fresh runtime values in each
-// evaluation, exactly as in the runtime-n kernel, so the CHUNK-INIT seeds stay runtime 0/1
-// values and the value channel is recomputed in every evaluation -- no folding or sharing of
-// seed-dependent work across evaluations (that is the separate NEXT-4 hoisted entry point).
+// compile-time constant, so the point, vector and result live in registers), but every
+// evaluation reads its row index and chunk start (from a per-CTA table) and the point's
+// coordinates (from the thread's own shared-memory copy) with VOLATILE shared loads: to both
+// compilers (NVVM and ptxas) they are fresh runtime values in each evaluation, exactly as in
+// the runtime-n kernel, so the CHUNK-INIT seeds stay runtime 0/1 values and the value channel
+// is recomputed in every evaluation -- no folding or sharing of work across evaluations (that
+// is the separate NEXT-4 hoisted entry point).  (Register moves through inline asm are not
+// enough: ptxas propagates them, folds the seeds and shares the evaluations -- measured, same
+// SASS for C = 1 and C = 2 at n = 2.)
 #pragma once
 #include <cstdint>
 
@@ -29,15 +32,15 @@
 
 namespace chessfad {
 
-// a copy the compiler cannot see through (volatile: never merged with another opq)
-CHF_INL int opq(int x) {
-  int r;
-  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(x));
+// shared-memory loads neither compiler may merge, hoist or fold
+CHF_INL double ld_vol(const double* p) {
+  double r;
+  asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(r) : "r"((uint32_t)__cvta_generic_to_shared(p)));
   return r;
 }
-CHF_INL double opq(double x) {
-  double r;
-  asm volatile("mov.b64 %0, %1;" : "=d"(r) : "d"(x));
+CHF_INL int2 ld_vol(const int2* p) {
+  int2 r;
+  asm volatile("ld.volatile.shared.v2.s32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"((uint32_t)__cvta_generic_to_shared(p)));
   return r;
 }
 
@@ -47,9 +50,9 @@ template <int C>
 struct RegSeed {
   static constexpr bool kStatic = true;  // variable loops fully unrolled (k compile-time)
   static constexpr bool kFused = true;   // the runtime-n kernel's forms (R5): same operations
-  const double* a;                       // this evaluation's opaque copy of the point
+  const double* a;                       // this evaluation's fresh copy of the point
   int stride;                            // 1
-  int i, cs;                             // opaque row / chunk start
+  int i, cs;                             // row / chunk start (runtime values)
   const double* sin2pi;                  // Ackley: sincos(2 pi a_k) of the point (registers)
   const double* cos2pi;
   CHF_INL hd<C> operator()(int k) const {
@@ -100,7 +103,9 @@ template <int NS>
 struct StreamCfg {
   static constexpr int kStages = NS == 2 ? 4 : 2;  // tiles in flight per CTA
   static constexpr size_t kTileBytes = (size_t)kStreamTP * NS * sizeof(double);
-  static constexpr size_t kSmem = 2 * kStages * kTileBytes + 8 * kStages + 16;  // points+vecs ring, barriers
+  static constexpr int kEvals = NS * NS;  // (row, chunk) table entries (C = 1 bound)
+  // points+vecs ring | the threads' point copies [NS][TP] | (i, cs) per evaluation | barriers
+  static constexpr size_t kSmem = 2 * kStages * kTileBytes + kTileBytes + 8 * kEvals + 8 * kStages + 16;
 };
 
 template <class F, int C, int NS>
@@ -111,8 +116,11 @@ __global__ void __launch_bounds__(kStreamTP, NS == 8 ? 1 : 2) hvp_stream_kernel(
   constexpr bool TRIG = uses_trig2pi<F>::value;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);  // stage s: points [TP*NS] | vecs [TP*NS]
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + 2 * S * Cfg::kTileBytes);
+  double* acopy = reinterpret_cast<double*>(smem_raw + 2 * S * Cfg::kTileBytes);  // [NS][TP]
+  int2* evtab = reinterpret_cast<int2*>(smem_raw + (2 * S + 1) * Cfg::kTileBytes);  // [NS * NS / C]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (2 * S + 1) * Cfg::kTileBytes + 8 * Cfg::kEvals);
   const int tid = threadIdx.x;
+  for (int q = tid; q < NS * (NS / C); q += blockDim.x) evtab[q] = make_int2(q / (NS / C), (q % (NS / C)) * C);
   const int64_t ntiles = (p.m + kStreamTP - 1) / kStreamTP;
 
   auto issue = [&](int64_t tile, int s) {  // one thread: bulk-copy tile's points and vectors
@@ -170,6 +178,8 @@ __global__ void __launch_bounds__(kStreamTP, NS == 8 ? 1 : 2) hvp_stream_kernel(
 #pragma unroll
       for (int k = 0; k < NS; k++) sincos(6.283185307179586 * a[k], ts + k, tc + k);
     }
+#pragma unroll
+    for (int k = 0; k < NS; k++) acopy[k * kStreamTP + tid] = a[k];  // this thread's slots only
     double out[NS];
 #pragma unroll
     for (int i = 0; i < NS; i++) {
@@ -178,8 +188,9 @@ __global__ void __launch_bounds__(kStreamTP, NS == 8 ? 1 : 2) hvp_stream_kernel(
       for (int j = 0; j < NS / C; j++) {
         double ao[NS];
 #pragma unroll
-        for (int k = 0; k < NS; k++) ao[k] = opq(a[k]);
-        const RegSeed<C> y{ao, 1, opq(i), opq(j * C), ts, tc};
+        for (int k = 0; k < NS; k++) ao[k] = ld_vol(acopy + k * kStreamTP + tid);
+        const int2 ic = ld_vol(evtab + i * (NS / C) + j);  // == (i, j C), opaque
+        const RegSeed<C> y{ao, 1, ic.x, ic.y, ts, tc};
         const hd<C> t = f.template operator()<C>(NS, y);  // CHUNK-INIT + f<hDual<C>>, Alg 7 :389-390
 #pragma unroll
         for (int l = 0; l < C; l++) res = res + t.v[C + 2 + l] * v[j * C + l];  // :392-394
