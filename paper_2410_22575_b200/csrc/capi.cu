@@ -179,10 +179,13 @@ cudaError_t dispatch_stream(int C, const BatchArgs& a, cudaStream_t s) {
 }
 
 // the stream kernel is used where it measured faster than the runtime-n kernel at m = 2^24
-// (profiles/r02/d/ab: 1.5-6x, except Ackley n = 8 with C <= 2: 1.2-1.4x slower, register-bound)
+// (profiles/r02/g): n = 2 (HBM-bound: 2.5-3.4x) and n = 4 (1.3-2.7x) for every function; at
+// n = 8 only prodsum (1.3x) -- Rosenbrock / Ackley at n = 8 are FP64-bound and the lane-per-
+// point register kernel executes them better (up to 1.5x)
 bool stream_small_n(int func, int n, int C) {
-  if (!CHF_STREAM_SMALL || !(n == 2 || n == 4 || n == 8)) return false;
-  return !(func == CHESSFAD_ACKLEY && n == 8 && C <= 2);
+  (void)C;
+  if (!CHF_STREAM_SMALL) return false;
+  return n == 2 || n == 4 || (n == 8 && func == CHESSFAD_PRODSUM);
 }
 
 bool aligned16(const BatchArgs& a) {

@@ -208,6 +208,7 @@ def test_kernel_path_introspection():
     assert chf.path("fletcher_powell", 16, 4, "hvp_seedsparse") == "f3_seedsparse"
     assert chf.path("rosenbrock", 2, 1) == "stream"
     assert chf.path("rosenbrock", 16, 16) == "reg"
-    assert chf.path("ackley", 8, 1) == "reg" and chf.path("ackley", 8, 4) == "stream"
+    assert chf.path("ackley", 8, 1) == "reg" and chf.path("prodsum", 8, 4) == "stream"
+    assert chf.path("ackley", 4, 1) == "stream" and chf.path("rosenbrock", 8, 8) == "reg"
     assert chf.path("rosenbrock", 8, 2, "hvp_hoisted") == "small_hoisted"
     assert chf.path("rosenbrock", 3, 2) == "unsupported"
