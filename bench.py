@@ -538,6 +538,8 @@ def executed_entry(func, n, C, src_hash, algo="hvp", path=None):
     ent = dict(ent)
     import paper_2410_22575_b200 as chf
     from paper_2410_22575_b200.sass import sass_hash_for
+    if not kernel_matches_path(ent.get("kernel", ""), chf.path(func, n, C, algo if algo in chf.ALGOS else "hvp")):
+        return None  # measured on a kernel family this call no longer runs
     cur = sass_hash_for(chf.LIB_PATH, ent["kernel"]) if ent.get("kernel") and ent.get("sass_hash") else None
     if cur is not None and cur == ent["sass_hash"]:
         ent["basis"] = f"ncu on identical kernel SASS ({cur})"
@@ -559,6 +561,20 @@ def _round(x):
     if isinstance(x, list):
         return [_round(v) for v in x]
     return x
+
+
+KERNEL_FAMILY = {"hvp_f3_mma_kernel": "f3_dmma", "hvp_f3_sparse_kernel": "f3_seedsparse", "hvp_f3_kernel": "f3_simt",
+                 "hvp_stream_kernel": "stream", "hvp_small_kernel": "small_hoisted"}
+
+
+def kernel_matches_path(kernel: str, path: str) -> bool:
+    """Does a profiled kernel (demangled name) belong to the family chessfad_path reports?"""
+    for prefix, fam in KERNEL_FAMILY.items():
+        if prefix + "<" in kernel:
+            return fam == path
+    if "hvp_reg_kernel<" in kernel:
+        return path == ("reg_seedsparse" if "SparseFunc" in kernel else "reg")
+    return False
 
 
 class _Null:

@@ -11,9 +11,14 @@ def test_executed_entry_current_and_stale(tmp_path):
     model = chf.model_flops_per_point("rosenbrock", 16, 16)
     tab = {"src_hash": "abc", "entries": {
         "rosenbrock n=16 C=16": {"executed_flops_per_point": 0.5 * model, "model_flops_per_point": model,
-                                 "fp64_pipe_active_pct": 80.0, "dram_bytes_per_launch": 1.0, "m": 1},
+                                 "fp64_pipe_active_pct": 80.0, "dram_bytes_per_launch": 1.0, "m": 1,
+                                 "kernel": "void hvp_reg_kernel<BuiltinFunc<0>, 16, 0, 4>(BatchArgs, T1)"},
         "fletcher_powell n=16 C=4 sym_hvp": {"executed_flops_per_point": 10.0, "model_flops_per_point": 20.0,
-                                             "fp64_pipe_active_pct": 60.0, "dram_bytes_per_launch": 1.0, "m": 1}}}
+                                             "fp64_pipe_active_pct": 60.0, "dram_bytes_per_launch": 1.0, "m": 1,
+                                             "kernel": "void hvp_f3_mma_kernel<16, 2>(BatchArgs)"},
+        "fletcher_powell n=16 C=8": {"executed_flops_per_point": 10.0, "model_flops_per_point": 20.0,
+                                     "fp64_pipe_active_pct": 60.0, "dram_bytes_per_launch": 1.0, "m": 1,
+                                     "kernel": "void hvp_f3_kernel<16, 0, 1, 0>(BatchArgs, const double2 *)"}}}
     p = tmp_path / "t.json"
     p.write_text(json.dumps(tab))
     e = bench.executed_entry("rosenbrock", 16, 16, "abc", path=str(p))
@@ -21,6 +26,10 @@ def test_executed_entry_current_and_stale(tmp_path):
     s = bench.executed_entry("rosenbrock", 16, 16, "other", path=str(p))
     assert s["basis"].startswith("STALE") and abs(s["executed_flops_per_point"] - 0.5 * model) < 1e-6
     assert bench.executed_entry("fletcher_powell", 16, 4, "abc", algo="sym_hvp", path=str(p)) is not None
+    # measured on the SIMT F3 kernel, but n = 16 now runs on the tensor-core kernel: not used
+    assert bench.executed_entry("fletcher_powell", 16, 8, "abc", path=str(p)) is None
+    assert bench.kernel_matches_path("void hvp_stream_kernel<BuiltinFunc<0>, 1, 2>(BatchArgs, T1)", "stream")
+    assert not bench.kernel_matches_path("void hvp_reg_kernel<SparseFunc<0>, 1, 0, 4>(BatchArgs, T1)", "reg")
     assert bench.executed_entry("ackley", 16, 16, "abc", path=str(p)) is None
     assert bench.executed_entry("ackley", 16, 16, "abc", path=str(tmp_path / "missing.json")) is None
 
