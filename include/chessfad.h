@@ -201,11 +201,11 @@ int chessfad_hvp_batch_paper(int level, int func, int n, int csize, int64_t m, c
 size_t chessfad_hvp_host_workspace_bytes(int func, int n, int64_t m, int64_t piece_points);
 
 /* 1 if (func, n, csize) runs for both chessfad_hvp_batch and chessfad_hessian_batch, else 0
- * (argument errors also give 0).  Compiled set: Fletcher-
- * Powell any csize | n, n <= 32 or (n <= 128 and n % 8 == 0); the other functions n <= 256 (Ackley n <= 176), with one
- * hDual<csize> per evaluation for csize in {1,2,4,8,16} and, for any other csize | n, csize/c'
- * column groups of the largest c' in {1,2,4,8,16} dividing csize (bit-identical results by
- * slot independence; slots 0/1 recomputed per group). */
+ * (argument errors also give 0).  Compiled set: Fletcher-Powell any csize | n, n <= 128 (every
+ * entry point); the other functions n <= 256 (Ackley n <= 176), with one hDual<csize> per
+ * evaluation for csize in {1,2,4,8,16} and, for any other csize | n, csize/c' column groups of
+ * the largest c' in {1,2,4,8,16} dividing csize (bit-identical results by slot independence,
+ * SPEC.md:107; slots 0/1 recomputed per group). */
 int chessfad_is_supported(int func, int n, int csize);
 
 /* algorithm ids for chessfad_is_supported_algo / chessfad_model_flops_per_point_algo */
@@ -253,7 +253,7 @@ int chessfad_fp64_probe(int blocks, int64_t iters, double *sink, void *stream);
  * DESIGN.md §3 describes each): "reg" (hDual<C> in registers, lane = point, warp = row),
  * "stream" (n in {2,4,8}, thread per point, bulk-copy ring; 16-byte-aligned buffers, else
  * "reg"), "small_hoisted", "reg_seedsparse", "f3_dmma" (Fletcher-Powell E-sums on the FP64
- * tensor core), "f3_simt", "f3_seedsparse", or "unsupported".  Static string, never NULL.
+ * tensor core), "f3_seedsparse", or "unsupported".  Static string, never NULL.
  */
 const char *chessfad_path(int func, int n, int csize, int algo);
 

@@ -17,7 +17,7 @@ using namespace chessfad;
 namespace {
 
 constexpr int kMaxNReg = 256;  // register-hDual path: (3 or 5)*n*33*8 B of shared memory per CTA
-constexpr int kMaxNF3 = 128;   // F3 path: per-thread R0/R1 scratch of 128 doubles
+constexpr int kMaxNF3 = 128;   // F3: tensor-core kernel tiles (f3_mma.cuh), seed-sparse tiles
 
 // hDual<32> needs > 255 registers (ptxas spills 400+ B) and measured ~25% slower than two
 // 16-column groups (profiles/r01/campaign1/time_cfg3n*.jsonl), so C >= 32 runs as groups of 16.
@@ -58,22 +58,11 @@ int validate(int func, int n, int csize, int64_t m, bool need_params_ptr, const 
 
 constexpr size_t kSmemMax = 227 * 1024;
 
-#ifndef CHF_F3_MMA
-#define CHF_F3_MMA 1  // F3 at n in {8, 16, ..., 64} on the FP64 tensor core (0: SIMT slot-column kernel)
-#endif
-#ifndef CHF_F3_MMA_MINN
-#define CHF_F3_MMA_MINN 5  // smaller n: the SIMT kernel (padding to 8 would multiply the E-sum work)
-#endif
-bool f3_mma_n(int n) { return CHF_F3_MMA && n >= CHF_F3_MMA_MINN && n <= 128; }
-
 int supported(int func, int n, int csize, int mode) {
   (void)csize;  // every C | n runs (F3: runtime C; register path: reg_kernel_chunk)
   if (mode == MODE_HVP_ROWHOIST) mode = MODE_HVP;  // same shapes as the per-evaluation HVP
-  if (func == CHESSFAD_FLETCHER_POWELL && f3_mma_n(n))  // tensor-core kernel: every mode
-    return F3Mma<64, MODE_SYM_HVP>::smem_bytes() <= kSmemMax && F3Mma<128, MODE_SYM_HVP>::smem_bytes() <= kSmemMax;
-  if (func == CHESSFAD_FLETCHER_POWELL)  // n > 32 streams (A, B) in 8-column cp.async stages
-    return n <= kMaxNF3 && (n <= 32 || n % kF3RingJ == 0) &&
-           f3_smem_bytes(n, groups_for(n, kWarpsF3, mode), mode) <= kSmemMax;
+  if (func == CHESSFAD_FLETCHER_POWELL)  // tensor-core kernel, every mode (smem fits at NN = 128)
+    return n <= kMaxNF3 && F3Mma<128, MODE_SYM_HVP>::smem_bytes() <= kSmemMax;
   return n <= kMaxNReg && reg_smem_bytes(func == CHESSFAD_ACKLEY, n, groups_for(n, kWarpsReg, mode), mode) <= kSmemMax;
 }
 
@@ -145,16 +134,6 @@ int sparse_entry(int func, int n, int csize, int64_t m, const double* points, co
 #undef CHF_CASE_SP
   }
   return e == cudaSuccess ? CHESSFAD_OK : CHESSFAD_ERR_CUDA;
-}
-
-// largest power of two <= 16 that divides n: the F3 k-block
-#ifndef CHF_F3_KBMAX
-#define CHF_F3_KBMAX 16  // F3 k-block cap (tuning knob; 8 measured 13-17% slower at n = 16 / 32)
-#endif
-int f3_kb(int n) {
-  int kb = CHF_F3_KBMAX;
-  while (n % kb) kb >>= 1;
-  return kb;
 }
 
 template <int F>
@@ -235,23 +214,15 @@ cudaError_t dispatch_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s)
   return cudaErrorInvalidValue;
 }
 
+// F3: the tensor-core kernel for NN = n rounded up to a multiple of 8 (f3_mma.cuh)
 template <int MODE>
 cudaError_t dispatch_f3(const BatchArgs& a, cudaStream_t s) {
-  if (f3_mma_n(a.n)) {
-    switch ((a.n + 7) / 8 * 8) {
+  switch ((a.n + 7) / 8 * 8) {
 #define CHF_MMA_CASE(NN) \
   case NN: return launch_f3_mma<NN, MODE>(a, s);
-      CHF_FOR_MMA_NN(CHF_MMA_CASE)
+    CHF_FOR_MMA_NN(CHF_MMA_CASE)
 #undef CHF_MMA_CASE
-    }
   }
-  const bool ab_smem = f3_ab_smem(a.n);
-#define CHF_CASE_KB(KB) \
-  case KB: return ab_smem ? launch_f3<KB, MODE, true>(a, s) : launch_f3<KB, MODE, false>(a, s);
-  switch (f3_kb(a.n)) {
-    CHF_CASE_KB(1) CHF_CASE_KB(2) CHF_CASE_KB(4) CHF_CASE_KB(8) CHF_CASE_KB(16)
-  }
-#undef CHF_CASE_KB
   return cudaErrorInvalidValue;
 }
 
@@ -570,7 +541,7 @@ const char* chessfad_path(int func, int n, int csize, int algo) {
   const bool sparse = algo == CHESSFAD_ALGO_HVP_SEEDSPARSE || algo == CHESSFAD_ALGO_HESSIAN_SEEDSPARSE;
   if (func == CHESSFAD_FLETCHER_POWELL) {
     if (sparse) return "f3_seedsparse";
-    return f3_mma_n(n) ? "f3_dmma" : "f3_simt";
+    return "f3_dmma";
   }
   if (sparse) return "reg_seedsparse";
   const int C = reg_kernel_chunk(csize);

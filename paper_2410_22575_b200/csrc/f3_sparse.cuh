@@ -19,12 +19,14 @@
 // the work per point drops from O(n^4 / C) to O(n^3).  Executed FLOPs are far below the §V
 // model; rates against the model are "effective".
 //
-// Mapping: as hvp_f3_kernel (lane = point, warp = row, CTA = 4 warps sharing a tile).  Per
+// Mapping: lane = point, warp = row, CTA = 4 warps sharing a tile (as the register kernel).  Per
 // row, columns go in blocks of CB (accumulators and the lane's sin/cos of the block in
 // registers); the inner loop over k reads (A_kj, B_kj) for the block's columns as warp-uniform
-// 16-byte broadcasts from ab[k][j] (interleaved, row-major: contiguous in j), from shared
-// memory for n <= 32 and through the read-only path otherwise.
+// broadcasts of (A_kj, B_kj): an interleaved row-major shared-memory copy for n <= 32, the
+// caller's params through the read-only path otherwise (no per-call scratch copy).
 #pragma once
+#include <type_traits>
+
 #include "kernels.cuh"
 
 #ifndef CHF_SP_KUNROLL
@@ -41,6 +43,38 @@ namespace chessfad {
 
 constexpr int kSpKUnroll = CHF_SP_KUNROLL;
 
+CHF_INL void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem_src));
+}
+CHF_INL void cp_async8(void* smem_dst, const void* gmem_src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem_src));
+}
+CHF_INL void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+CHF_INL void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// (A_kj, B_kj) pairs: from the caller's params directly (global, read-only path; no scratch
+// copy) or from an interleaved shared-memory copy [k][j] (n <= 32)
+struct ABGlobal {
+  const double* A;
+  const double* B;
+  int n;
+  CHF_INL double2 operator()(int k, int j) const {
+    return make_double2(__ldg(A + (size_t)k * n + j), __ldg(B + (size_t)k * n + j));
+  }
+  CHF_INL void stage(double2* dst, int k, int j) const {  // cp.async of one pair into an interleaved slot
+    cp_async8(&dst->x, A + (size_t)k * n + j);
+    cp_async8(&dst->y, B + (size_t)k * n + j);
+  }
+};
+struct ABSmem {
+  const double2* ab;
+  int n;
+  CHF_INL double2 operator()(int k, int j) const { return ab[k * n + j]; }
+};
+
 // The j = 0 term of each E chain is written `A x + B y` (f3_fma's FIRST form) and every later
 // term as fma(B, y, fma(A, x, E)); the sparse terms below copy whichever form the full chain
 // used for that j so that nvcc rounds them identically.
@@ -51,8 +85,8 @@ CHF_INL double f3_sp_term(double A, double x, double B, double y) {
 }
 
 // one block of CB columns [cb, cb + CB) of row i: fC[q] = d2f/dx_i dx_{cb+q} for col != i
-template <int CB, bool ROW0, bool COL0>
-CHF_INL void f3_sp_block(int n, int i, int cb, double si, double ci, const double2* __restrict__ ab,
+template <int CB, bool ROW0, bool COL0, class AB>
+CHF_INL void f3_sp_block(int n, int i, int cb, double si, double ci, const AB& ab,
                          const double* __restrict__ sa, const double* __restrict__ ca, double (&fC)[CB]) {
   double sc[CB], cc[CB];
 #pragma unroll
@@ -62,12 +96,11 @@ CHF_INL void f3_sp_block(int n, int i, int cb, double si, double ci, const doubl
   }
 #pragma unroll kSpKUnroll
   for (int k = 0; k < n; k++) {
-    const double2 c1 = ab[k * n + i];
+    const double2 c1 = ab(k, i);
     const double r1 = -f3_sp_term<ROW0>(c1.x, ci, c1.y, -si);  // slot 1: the j = i term
-    const double2* abk = ab + k * n + cb;
 #pragma unroll
     for (int q = 0; q < CB; q++) {
-      const double2 c = abk[q];
+      const double2 c = ab(k, cb + q);
       const double r2 = (COL0 && q == 0) ? -f3_sp_term<true>(c.x, cc[q], c.y, -sc[q])
                                          : -f3_sp_term<false>(c.x, cc[q], c.y, -sc[q]);  // slot 2+c
       const double t = __dmul_rn(r1, r2);
@@ -113,7 +146,7 @@ CHF_INL void f3_sp_stage(int k0, double si, double ci, const double2* __restrict
 // row 0 / column block 0 take other term forms), so row0 / col0 are runtime (warp-uniform)
 // flags here and only the barrier-free stage compute is specialised.
 template <int CB>
-CHF_INL void f3_sp_block_staged(int n, int i, int cb, bool row0, double si, double ci, const double2* __restrict__ ab,
+CHF_INL void f3_sp_block_staged(int n, int i, int cb, bool row0, double si, double ci, const ABGlobal& ab,
                                 const SpRing& rg, const double* __restrict__ sa, const double* __restrict__ ca,
                                 double (&fC)[CB]) {
   double sc[CB], cc[CB];
@@ -128,9 +161,9 @@ CHF_INL void f3_sp_block_staged(int n, int i, int cb, bool row0, double si, doub
     const int k0 = st * kSpKS, buf = st & 1;
     for (int q = threadIdx.x; q < kSpKS * CB; q += blockDim.x) {
       const int kk = q / CB, cq = q - kk * CB;
-      cp_async16(rg.blk + (buf * kSpKS + kk) * CB + cq, ab + (size_t)(k0 + kk) * n + cb + cq);
+      ab.stage(rg.blk + (buf * kSpKS + kk) * CB + cq, k0 + kk, cb + cq);
     }
-    if (lane < kSpKS) cp_async16(rg.col + buf * kSpKS + lane, ab + (size_t)(k0 + lane) * n + i);
+    if (lane < kSpKS) ab.stage(rg.col + buf * kSpKS + lane, k0 + lane, i);
     cp_async_commit();
   };
   __syncthreads();  // every warp is done with the previous block's buffers
@@ -154,13 +187,13 @@ CHF_INL void f3_sp_block_staged(int n, int i, int cb, bool row0, double si, doub
 
 // row i: out_i = sum_col d2f/dx_i dx_col * v_col, ascending columns (HVP), or the row stored
 // to hrow (HESS; nullptr for ragged-tail lanes)
-template <bool ROW0>
-CHF_INL double f3_sp_diag(int n, int i, double si, double ci, const double2* __restrict__ ab,
+template <bool ROW0, class AB>
+CHF_INL double f3_sp_diag(int n, int i, double si, double ci, const AB& ab,
                           const double* __restrict__ r0t) {
   // diagonal column: the full slot set (r0, r1 = r2, rC), f3_phase_b's expression
   double fdiag = 0.0;
   for (int k = 0; k < n; k++) {
-    const double2 c = ab[k * n + i];
+    const double2 c = ab(k, i);
     const double r0 = r0t[k * kPad];
     const double r1 = -f3_sp_term<ROW0>(c.x, ci, c.y, -si);
     const double r2 = r1;
@@ -174,8 +207,8 @@ CHF_INL double f3_sp_diag(int n, int i, double si, double ci, const double2* __r
 }
 
 // row0 is a runtime flag so that the staged path's barriers are shared by all warps
-template <int CB, bool HESS, bool STAGED>
-CHF_INL double f3_sp_row(int n, int i, bool row0, const double2* __restrict__ ab, const double* __restrict__ sa,
+template <int CB, bool HESS, bool STAGED, class AB>
+CHF_INL double f3_sp_row(int n, int i, bool row0, const AB& ab, const double* __restrict__ sa,
                          const double* __restrict__ ca, const double* __restrict__ r0t, const double* __restrict__ v,
                          int vs, double* __restrict__ hrow, const SpRing& rg) {
   const double si = sa[i * kPad], ci = ca[i * kPad];
@@ -211,7 +244,7 @@ CHF_INL double f3_sp_row(int n, int i, bool row0, const double2* __restrict__ ab
 // STAGED (SLIM, n % kSpKS == 0): the CTA-shared (A, B) block rows go through the cp.async
 // double buffer (f3_sp_block_staged); every warp then has n / 4 rows (uniform barriers).
 template <int CB, bool AB_SMEM, bool SLIM, bool HESS, bool STAGED>
-__global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? CHF_SP_MINB_SMEM : CHF_SP_MINB) hvp_f3_sparse_kernel(BatchArgs p, const double2* __restrict__ ab_g) {
+__global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? CHF_SP_MINB_SMEM : CHF_SP_MINB) hvp_f3_sparse_kernel(BatchArgs p) {
   extern __shared__ double smem[];
   const int n = p.n, G = p.groups, P = 32 * G;
   double* s_sa = smem;                 // [G][n][33]  sin a
@@ -236,7 +269,10 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? CHF_SP_MINB_SMEM : CH
     s_ca[idx] = c;
   }
   __syncthreads();
-  const double2* ab = AB_SMEM ? s_ab : ab_g;
+  using AB = typename std::conditional<AB_SMEM, ABSmem, ABGlobal>::type;
+  AB ab;
+  if constexpr (AB_SMEM) ab = ABSmem{s_ab, n};
+  else ab = ABGlobal{p.params, p.params + (size_t)n * n, n};
   const double* Es = p.params + 2 * (size_t)n * n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = warp % G, wg = warp / G, rstep = kWarpsF3 / G;
@@ -247,11 +283,11 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? CHF_SP_MINB_SMEM : CH
   for (int k = wg; k < n; k += rstep) {
     double E;
     {
-      const double2 c = ab[k * n];
+      const double2 c = ab(k, 0);
       E = c.x * sa[0] + c.y * ca[0];
     }
     for (int j = 1; j < n; j++) {
-      const double2 c = ab[k * n + j];
+      const double2 c = ab(k, j);
       E = E + c.x * sa[j * kPad] + c.y * ca[j * kPad];
     }
     r0t[k * kPad] = Es[k] - E;
@@ -281,10 +317,5 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? CHF_SP_MINB_SMEM : CH
   }
 }
 
-// (A, B) -> interleaved row-major ab[k * n + j] = (A_kj, B_kj), n > 32
-static __global__ void f3_ab_interleave_kernel(int n, const double* __restrict__ params, double2* __restrict__ ab) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < n * n) ab[q] = make_double2(params[q], params[n * n + q]);
-}
 
 }  // namespace chessfad

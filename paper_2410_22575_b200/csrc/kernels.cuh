@@ -25,7 +25,6 @@
 #pragma once
 #include <cstdint>
 
-#include "f3.cuh"
 #include "testfuncs.cuh"
 
 namespace chessfad {
@@ -53,7 +52,7 @@ struct BatchArgs {
 };
 
 constexpr int kPad = 33;     // shared-memory row stride (doubles) of [k][lane] tiles
-constexpr int kWarpsF3 = 4;  // Fletcher-Powell path: 128 threads per CTA
+constexpr int kWarpsF3 = 4;  // seed-sparse Fletcher-Powell kernel: 128 threads per CTA
 
 // stage points [and vectors] of the tile into shared memory, transposed per 32-point group
 CHF_INL void stage_tile(const BatchArgs& p, int64_t e0, int P, double* s_pts, double* s_vec) {
@@ -221,125 +220,6 @@ __global__ void __launch_bounds__(128) hvp_small_kernel(BatchArgs p, F f) {
   double2* o2 = reinterpret_cast<double2*>(p.out + e * NS);
 #pragma unroll
   for (int q = 0; q < NS / 2; q++) o2[q] = make_double2(out[2 * q], out[2 * q + 1]);
-}
-
-// ---------------------------------------------------------------- F3 Fletcher-Powell
-// params = [A (n*n) | B (n*n) | E* (n)].  (A_kj, B_kj) are interleaved and transposed,
-// abT[j*n + k], so that the KB k-values of one j are 16-byte broadcast loads at immediate
-// offsets: in shared memory when AB_SMEM (n <= 32), else in a global scratch copy built by
-// f3_ab_prep_kernel.  SLIM (n > 32): only sin/cos tiles in shared memory; vectors are read
-// and outputs written straight from/to global memory so that 3 CTAs fit per SM.
-static __global__ void f3_ab_prep_kernel(int n, const double* __restrict__ params, double2* __restrict__ abT) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= n * n) return;
-  const int k = q / n, j = q - k * n;
-  abT[j * n + k] = make_double2(params[q], params[n * n + q]);
-}
-
-constexpr int kF3RingJ = 8;  // j-values per cp.async stage of the (A, B) ring (n > 32)
-
-// min CTAs/SM: 3 (<= 168 registers) with (A, B) in shared memory; 2 (<= 255) for the ring
-// path, whose 16 broadcast loads per j need registers to be batched ahead of their DFMAs
-#ifndef CHF_F3_SMEM_MINB
-#define CHF_F3_SMEM_MINB 3
-#endif
-template <int KB, int MODE, bool AB_SMEM, bool SLIM>
-__global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? CHF_F3_SMEM_MINB : 2)
-    hvp_f3_kernel(BatchArgs p, const double2* __restrict__ abT_g) {
-  constexpr bool HESS = mode_hess(MODE);
-  constexpr bool VEC_TILE = !HESS && !SLIM;
-  extern __shared__ double smem[];
-  const int n = p.n, G = p.groups, P = 32 * G, C = p.csize;
-  double* s_sa = smem;                 // [G][n][33]  sin a
-  double* s_ca = s_sa + G * n * kPad;  // [G][n][33]  cos a
-  double* s_vec = s_ca + G * n * kPad;
-  double* s_out = s_vec + G * n * kPad;
-  // (A, B): the whole matrix (AB_SMEM) or this CTA's per-warp cp.async rings
-  double2* s_ab = reinterpret_cast<double2*>((VEC_TILE || MODE == MODE_SYM_HVP) ? s_out + G * n * kPad : s_vec);
-  const int64_t e0 = (int64_t)blockIdx.x * P;
-  stage_tile(p, e0, P, s_sa, VEC_TILE ? s_vec : nullptr);
-  if (MODE == MODE_SYM_HVP)
-    for (int q = threadIdx.x; q < G * n * kPad; q += blockDim.x) s_out[q] = 0.0;
-  if (AB_SMEM) {
-    const double* A = p.params;
-    const double* B = p.params + (size_t)n * n;
-    for (int q = threadIdx.x; q < n * n; q += blockDim.x) {
-      const int k = q / n, j = q - k * n;
-      s_ab[j * n + k] = make_double2(A[q], B[q]);  // transposed: [j][k]
-    }
-  }
-  __syncthreads();
-  // g, g', g'' of the seeded inputs: sin a_k, cos a_k once per tile (see f3.cuh)
-  for (int q = threadIdx.x; q < G * n * 32; q += blockDim.x) {
-    const int idx = (q >> 5) * kPad + (q & 31);
-    double s, c;
-    sincos(s_sa[idx], &s, &c);
-    s_sa[idx] = s;
-    s_ca[idx] = c;
-  }
-  __syncthreads();
-
-  const double* Es = p.params + 2 * (size_t)n * n;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = warp % G, rstep = kWarpsF3 / G;
-  const double* sa = s_sa + g * n * kPad + lane;
-  const double* ca = s_ca + g * n * kPad + lane;
-  const int64_t e = e0 + g * 32 + lane;
-  const int64_t ec = e < p.m ? e : p.m - 1;
-  // vector column of this lane: shared tile (stride kPad) or global row (stride 1)
-  const double* v = HESS ? nullptr : (VEC_TILE ? s_vec + g * n * kPad + lane : p.vecs + ec * n);
-  double* o = (HESS || SLIM) ? nullptr : s_out + g * n * kPad + lane;
-  const int nchunk = n / C;
-  const ABRing<KB, kF3RingJ> ring{s_ab + warp * 2 * kF3RingJ * KB, abT_g, n, lane};
-  double R0[128], R1[128];  // per-thread residual slots 0/1 of one evaluation (n <= 128 used)
-  for (int i = warp / G; i < n; i += rstep) {
-    const int scn = i / C;
-    RowSink<MODE> sink = make_sink<MODE>(p, i, e, v, o, VEC_TILE ? kPad : 1);
-    if (MODE == MODE_HESS_GRAD) {  // gradient: slot 1 of f = sum_k r_k r_k
-      // every lane runs phase A (the (A, B) ring is filled and __syncwarp'ed by all 32 lanes;
-      // tail lanes hold a replicated point); only the store is guarded
-      if (AB_SMEM)
-        f3_phase_a<KB>(n, i, sa, ca, kPad, ABShared{s_ab, n}, Es, R0, R1);
-      else
-        f3_phase_a<KB>(n, i, sa, ca, kPad, ring, Es, R0, R1);
-      double f1 = 0.0;
-      for (int k = 0; k < n; k++) {
-        const double rr1 = R0[k] * R1[k] + R0[k] * R1[k];  // (r*r)[1] = r0 r1 + r0 r1 (Fig. 1)
-        f1 = (k == 0) ? rr1 : f1 + rr1;
-      }
-      if (e < p.m) p.grad[e * n + i] = f1;
-    }
-    if (MODE == MODE_HVP_ROWHOIST) {  // NEXT-4: phase A once per row
-      if (AB_SMEM)
-        f3_phase_a<KB>(n, i, sa, ca, kPad, ABShared{s_ab, n}, Es, R0, R1);
-      else
-        f3_phase_a<KB>(n, i, sa, ca, kPad, ring, Es, R0, R1);
-    }
-    for (int j = mode_sym(MODE) ? scn : 0; j < nchunk; j++) {
-      sink.mirror = j > scn;
-      if (MODE == MODE_HVP_ROWHOIST) {
-        if (AB_SMEM)
-          f3_phase_b<KB>(n, C, i, j * C, sa, ca, kPad, ABShared{s_ab, n}, R0, R1, sink);
-        else
-          f3_phase_b<KB>(n, C, i, j * C, sa, ca, kPad, ring, R0, R1, sink);
-      } else if (AB_SMEM) {
-        f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ABShared{s_ab, n}, Es, R0, R1, sink);
-      } else {
-        f3_eval<KB>(n, C, i, j * C, sa, ca, kPad, ring, Es, R0, R1, sink);
-      }
-    }
-    if (!HESS) {
-      if (SLIM) {
-        if (e < p.m) p.out[e * n + i] = sink.res;
-      } else {
-        o[i * kPad] = sink.res;
-      }
-    }
-  }
-  if (!HESS && !SLIM) {
-    __syncthreads();
-    write_tile(p, e0, P, s_out);
-  }
 }
 
 }  // namespace chessfad

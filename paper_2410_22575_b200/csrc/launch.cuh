@@ -32,16 +32,7 @@ inline size_t reg_smem_bytes(bool trig, int n, int G, int mode) {
   return (size_t)tiles * G * n * kPad * sizeof(double);
 }
 
-inline bool f3_ab_smem(int n) { return n <= 32; }
-// slim tiles (no vector / output tiles) for n > 32; the symmetric HVP needs its output tile
-inline bool f3_slim(int n, int mode) { return n > 32 && mode != MODE_SYM_HVP; }
-
-inline size_t f3_smem_bytes(int n, int G, int mode) {
-  const int tiles = (mode_hess(mode) || f3_slim(n, mode)) ? 2 : 4;
-  const size_t ab = f3_ab_smem(n) ? (size_t)n * n * 2 * sizeof(double)                        // whole (A, B)
-                                  : (size_t)kWarpsF3 * 2 * kF3RingJ * 16 * 2 * sizeof(double);  // rings (KB <= 16)
-  return (size_t)tiles * G * n * kPad * sizeof(double) + ab;
-}
+inline bool f3_ab_smem(int n) { return n <= 32; }  // seed-sparse F3: (A, B) copied to shared memory
 
 template <class K, class... Args>
 inline cudaError_t launch_with_smem(K kernel, int grid, int block, size_t smem, cudaStream_t s, const Args&... args) {
@@ -68,29 +59,8 @@ cudaError_t launch_reg(BatchArgs a, cudaStream_t s) {
   return launch_functor<BuiltinFunc<FUNC>, C, MODE>(BuiltinFunc<FUNC>{}, a, s);
 }
 
-// n > 32: (A, B) interleaved + transposed into stream-ordered scratch, freed on the stream
-template <int KB, int MODE, bool AB_SMEM>
-cudaError_t launch_f3(BatchArgs a, cudaStream_t s) {
-  a.groups = groups_for(a.n, kWarpsF3, MODE);
-  const int64_t P = 32 * a.groups;
-  const int grid = (int)((a.m + P - 1) / P);
-  const size_t smem = f3_smem_bytes(a.n, a.groups, MODE);
-  if (AB_SMEM) return launch_with_smem(hvp_f3_kernel<KB, MODE, true, false>, grid, kWarpsF3 * 32, smem, s, a,
-                                       (const double2*)nullptr);
-  double2* abT = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&abT, (size_t)a.n * a.n * sizeof(double2), s);
-  if (e != cudaSuccess) return e;
-  f3_ab_prep_kernel<<<(a.n * a.n + 255) / 256, 256, 0, s>>>(a.n, a.params, abT);
-  e = f3_slim(a.n, MODE)
-          ? launch_with_smem(hvp_f3_kernel<KB, MODE, false, true>, grid, kWarpsF3 * 32, smem, s, a, (const double2*)abT)
-          : launch_with_smem(hvp_f3_kernel<KB, MODE, false, false>, grid, kWarpsF3 * 32, smem, s, a,
-                             (const double2*)abT);
-  const cudaError_t e2 = cudaFreeAsync(abT, s);
-  return e != cudaSuccess ? e : e2;
-}
-
 // NEXT-4 seed-sparse F3 HVP (f3_sparse.cuh): CB = column block, (A, B) in shared memory for
-// n <= 32, else an interleaved row-major scratch copy; SLIM tiles for n > 32
+// n <= 32, else read from the caller's params; SLIM tiles for n > 32
 inline bool f3_sp_slim(int n) { return n > 32; }
 inline bool f3_sp_staged(int n) { return f3_sp_slim(n) && n % kSpKS == 0; }
 inline size_t f3_sparse_smem_bytes(int n, int G) {
@@ -105,20 +75,9 @@ cudaError_t launch_f3_sparse(BatchArgs a, cudaStream_t s) {
   const int64_t P = 32 * a.groups;
   const int grid = (int)((a.m + P - 1) / P);
   const size_t smem = f3_sparse_smem_bytes(a.n, a.groups);
-  if (f3_ab_smem(a.n))
-    return launch_with_smem(hvp_f3_sparse_kernel<CB, true, false, HESS, false>, grid, kWarpsF3 * 32, smem, s, a,
-                            (const double2*)nullptr);
-  double2* ab = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&ab, (size_t)a.n * a.n * sizeof(double2), s);
-  if (e != cudaSuccess) return e;
-  f3_ab_interleave_kernel<<<(a.n * a.n + 255) / 256, 256, 0, s>>>(a.n, a.params, ab);
-  e = f3_sp_staged(a.n)
-          ? launch_with_smem(hvp_f3_sparse_kernel<CB, false, true, HESS, true>, grid, kWarpsF3 * 32, smem, s, a,
-                             (const double2*)ab)
-          : launch_with_smem(hvp_f3_sparse_kernel<CB, false, true, HESS, false>, grid, kWarpsF3 * 32, smem, s, a,
-                             (const double2*)ab);
-  const cudaError_t e2 = cudaFreeAsync(ab, s);
-  return e != cudaSuccess ? e : e2;
+  if (f3_ab_smem(a.n)) return launch_with_smem(hvp_f3_sparse_kernel<CB, true, false, HESS, false>, grid, kWarpsF3 * 32, smem, s, a);
+  return f3_sp_staged(a.n) ? launch_with_smem(hvp_f3_sparse_kernel<CB, false, true, HESS, true>, grid, kWarpsF3 * 32, smem, s, a)
+                           : launch_with_smem(hvp_f3_sparse_kernel<CB, false, true, HESS, false>, grid, kWarpsF3 * 32, smem, s, a);
 }
 #define CHF_FOR_CB(X) X(1) X(2) X(4) X(8) X(16)
 #define CHF_DECL_SP(CB) extern template cudaError_t launch_f3_sparse<CB, false>(BatchArgs, cudaStream_t); \
@@ -208,9 +167,5 @@ CHF_FOR_C(CHF_DECL_SPR1, FUNC_ROSENBROCK)
 CHF_FOR_C(CHF_DECL_SPR1, FUNC_ACKLEY)
 CHF_FOR_C(CHF_DECL_SPR1, FUNC_PRODSUM)
 
-#define CHF_DECL_F31(KB, AB, M) extern template cudaError_t launch_f3<KB, M, AB>(BatchArgs, cudaStream_t);
-#define CHF_DECL_F3(KB) CHF_FOR_MODE(CHF_DECL_F31, KB, false) CHF_FOR_MODE(CHF_DECL_F31, KB, true) \
-  CHF_DECL_F31(KB, false, MODE_HVP_ROWHOIST) CHF_DECL_F31(KB, true, MODE_HVP_ROWHOIST)
-CHF_DECL_F3(1) CHF_DECL_F3(2) CHF_DECL_F3(4) CHF_DECL_F3(8) CHF_DECL_F3(16)
 
 }  // namespace chessfad

@@ -204,7 +204,8 @@ def test_kernel_path_introspection():
     assert chf.path("fletcher_powell", 128, 8) == "f3_dmma"
     assert chf.path("fletcher_powell", 12, 4) == "f3_dmma"   # zero-padded to 16
     assert chf.path("fletcher_powell", 128, 8, "sym_hvp") == "f3_dmma"
-    assert chf.path("fletcher_powell", 4, 2) == "f3_simt"
+    assert chf.path("fletcher_powell", 4, 2) == "f3_dmma"    # zero-padded to 8
+    assert chf.path("fletcher_powell", 100, 4, "sym_hvp") == "f3_dmma"
     assert chf.path("fletcher_powell", 16, 4, "hvp_seedsparse") == "f3_seedsparse"
     assert chf.path("rosenbrock", 2, 1) == "stream"
     assert chf.path("rosenbrock", 16, 16) == "reg"
