@@ -62,7 +62,8 @@ int supported(int func, int n, int csize, int mode) {
   (void)csize;  // every C | n runs (F3: runtime C; register path: reg_kernel_chunk)
   if (mode == MODE_HVP_ROWHOIST) mode = MODE_HVP;  // same shapes as the per-evaluation HVP
   if (func == CHESSFAD_FLETCHER_POWELL)  // tensor-core kernel, every mode (smem fits at NN = 128)
-    return n <= kMaxNF3 && F3Mma<128, MODE_SYM_HVP>::smem_bytes() <= kSmemMax;
+    return n <= kMaxNF3 && F3Mma<128, MODE_SYM_HVP>::smem_bytes() <= kSmemMax &&
+           F3Mma<128, MODE_HVP>::smem_bytes() <= kSmemMax;
   return n <= kMaxNReg && reg_smem_bytes(func == CHESSFAD_ACKLEY, n, groups_for(n, kWarpsReg, mode), mode) <= kSmemMax;
 }
 

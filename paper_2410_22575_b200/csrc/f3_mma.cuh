@@ -57,7 +57,9 @@ constexpr int f3_mma_kb(int NN) {  // k rows of M per block: all of M up to n = 
 }
 template <int NN, int MODE>
 struct F3Mma {
-  static constexpr int W = NN <= 64 ? 8 : 4;
+  // 8 warps (64 points) whenever M's block and the 64 points' sin/cos tables fit: every n and
+  // mode except the symmetric HVP at n > 64, whose scatter tile needs the room (4 warps)
+  static constexpr int W = (NN <= 64 || MODE != MODE_SYM_HVP) ? 8 : 4;
   static constexpr int KB = f3_mma_kb(NN);
   static constexpr int P = W * kMmaPPW;        // points per CTA
   static constexpr int TS = P + 8;             // sin/cos table row stride (doubles): 2 wavefronts per LDS
