@@ -1,4 +1,4 @@
-// kernels.cuh -- batched HVP / Hessian kernels (sm_100a, FP64 SIMT, no tensor cores).
+// chessfad/kernels.cuh -- batched HVP / Hessian kernels (sm_100a, FP64 SIMT, no tensor cores).
 //
 // Work decomposition (the paper's L0/L1/L2 levels):
 // the paper maps instance x row x chunk to threads (Fig. 2: one thread per (e, i, j) and a

@@ -24,7 +24,7 @@
 
 #include <cstdint>
 
-#include "../paper_2410_22575_b200/csrc/launch.cuh"
+#include "chessfad/launch_functor.cuh"  // self-contained: include/ only
 
 namespace chessfad {
 

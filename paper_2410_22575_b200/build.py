@@ -35,7 +35,7 @@ def source_hash() -> str:
     that the ncu-measured executed-FLOP table (profiles/executed_flops.json) describes."""
     import hashlib
     h = hashlib.sha256()
-    for f in sorted(glob.glob(os.path.join(CSRC, "*.cu*"))) + [os.path.join(ROOT, "include", "chessfad.h")]:
+    for f in sorted(glob.glob(os.path.join(CSRC, "*.cu*"))) + _public_headers():
         h.update(os.path.basename(f).encode())
         h.update(open(f, "rb").read())
     h.update(" ".join(ARCH + NVCC_FLAGS[:-2]).encode())
@@ -46,8 +46,13 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+def _public_headers():
+    inc = os.path.join(ROOT, "include")
+    return [os.path.join(inc, "chessfad.h")] + sorted(glob.glob(os.path.join(inc, "chessfad", "*.cuh")))
+
+
 def _deps():
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu*"))) + [os.path.join(ROOT, "include", "chessfad.h"), __file__]
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu*"))) + _public_headers() + [__file__]
 
 
 def up_to_date() -> bool:

@@ -39,7 +39,7 @@
 // The sum over k of each second-order entry is a per-lane partial over the k-tiles plus a
 // 3-step butterfly over g; every other reduction order is as in the SIMT kernel.
 #pragma once
-#include "kernels.cuh"
+#include "chessfad/kernels.cuh"
 
 namespace chessfad {
 

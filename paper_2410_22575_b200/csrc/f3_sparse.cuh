@@ -27,7 +27,7 @@
 #pragma once
 #include <type_traits>
 
-#include "kernels.cuh"
+#include "chessfad/kernels.cuh"
 
 #ifndef CHF_SP_KUNROLL
 #define CHF_SP_KUNROLL 4  // k-loop unroll of the column-block loop (measured 4 > 2: profiles/r01/sparse/)

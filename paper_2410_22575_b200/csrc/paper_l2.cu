@@ -17,7 +17,7 @@
 #include <cstdint>
 
 #include "../../include/chessfad.h"
-#include "testfuncs.cuh"
+#include "chessfad/testfuncs.cuh"
 
 namespace chessfad {
 namespace {

@@ -28,7 +28,7 @@
 #pragma once
 #include <cstdint>
 
-#include "kernels.cuh"
+#include "chessfad/kernels.cuh"
 
 namespace chessfad {
 

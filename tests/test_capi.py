@@ -213,3 +213,20 @@ def test_kernel_path_introspection():
     assert chf.path("ackley", 4, 1) == "stream" and chf.path("rosenbrock", 8, 8) == "reg"
     assert chf.path("rosenbrock", 8, 2, "hvp_hoisted") == "small_hoisted"
     assert chf.path("rosenbrock", 3, 2) == "unsupported"
+
+
+def test_device_header_self_contained(tmp_path):
+    """include/chessfad_device.cuh (user functions, NEXT-3) compiles from include/ alone: a copy
+    of include/ outside the repo and the example translation unit, nothing else."""
+    import shutil
+    import subprocess
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not os.path.exists(nvcc):
+        pytest.skip("nvcc not available")
+    inc = tmp_path / "include"
+    shutil.copytree(os.path.join(ROOT, "include"), inc)
+    src = tmp_path / "user.cu"
+    shutil.copy(os.path.join(ROOT, "examples", "user_function.cu"), src)
+    r = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-std=c++17", "-O1", "-I", str(inc),
+                        "-c", str(src), "-o", str(tmp_path / "user.o")], capture_output=True, text=True, cwd=tmp_path)
+    assert r.returncode == 0, r.stderr[-3000:]
