@@ -146,6 +146,23 @@ int chessfad_hessian_batch_seedsparse(int func, int n, int csize, int64_t m, con
                                       const double *params, void *stream);
 
 /*
+ * Seed sparsity (as chessfad_hvp_batch_seedsparse) for the symmetric algorithms and the
+ * gradient by-product, Rosenbrock / Ackley / prodsum: Alg 8 SC-HESS-VEC,
+ * Alg 6 SCHUNK-HESS and Alg 5 + gradient, evaluating only the
+ * terms of each running sum that touch row i or the chunk (the others add exact +-0 to every
+ * derivative slot; the gradient slot v[1] needs only the terms touching i).  Arguments,
+ * layouts and results as chessfad_sym_hvp_batch / chessfad_sym_hessian_batch /
+ * chessfad_hessian_grad_batch (bit-identical up to the sign of zero); executed FLOPs below the
+ * model.  Fletcher-Powell: ERR_UNSUPPORTED (its seed-sparse kernel implements Alg 7 / Alg 5).
+ */
+int chessfad_sym_hvp_batch_seedsparse(int func, int n, int csize, int64_t m, const double *points,
+                                      const double *vecs, double *out, const double *params, void *stream);
+int chessfad_sym_hessian_batch_seedsparse(int func, int n, int csize, int64_t m, const double *points,
+                                          double *hess, const double *params, void *stream);
+int chessfad_hessian_grad_batch_seedsparse(int func, int n, int csize, int64_t m, const double *points,
+                                           double *hess, double *grad, const double *params, void *stream);
+
+/*
  * End-to-end variant of chessfad_hvp_batch on HOST buffers: points, vecs, out (m x n) and
  * params are HOST pointers (pinned memory gives copy/compute overlap; pageable memory
  * works but serialises).  The batch is split into pieces of `piece_points` points
@@ -216,8 +233,11 @@ enum chessfad_algo {
   CHESSFAD_ALGO_SYM_HESSIAN = 3,  /* Alg 6, chessfad_sym_hessian_batch */
   CHESSFAD_ALGO_HVP_HOISTED = 4,  /* Alg 7 + NEXT-4 value-channel hoisting, chessfad_hvp_batch_hoisted */
   CHESSFAD_ALGO_HESSIAN_GRAD = 5, /* Alg 5 + gradient by-product, chessfad_hessian_grad_batch */
-  CHESSFAD_ALGO_HVP_SEEDSPARSE = 6, /* Alg 7 + NEXT-4 seed sparsity (F3), chessfad_hvp_batch_seedsparse */
-  CHESSFAD_ALGO_HESSIAN_SEEDSPARSE = 7 /* Alg 5 + seed sparsity (F3), chessfad_hessian_batch_seedsparse */
+  CHESSFAD_ALGO_HVP_SEEDSPARSE = 6, /* Alg 7 + NEXT-4 seed sparsity, chessfad_hvp_batch_seedsparse */
+  CHESSFAD_ALGO_HESSIAN_SEEDSPARSE = 7, /* Alg 5 + seed sparsity, chessfad_hessian_batch_seedsparse */
+  CHESSFAD_ALGO_SYM_HVP_SEEDSPARSE = 8, /* Alg 8 + seed sparsity (F1/F2/F4), chessfad_sym_hvp_batch_seedsparse */
+  CHESSFAD_ALGO_SYM_HESSIAN_SEEDSPARSE = 9, /* Alg 6 + seed sparsity (F1/F2/F4), chessfad_sym_hessian_batch_seedsparse */
+  CHESSFAD_ALGO_HESSIAN_GRAD_SEEDSPARSE = 10 /* Alg 5 + gradient + seed sparsity (F1/F2/F4) */
 };
 
 /* 1 if (func, n, csize) runs for the given algorithm, else 0. */

@@ -19,14 +19,15 @@ FUNCS = {"rosenbrock": ROSENBROCK, "ackley": ACKLEY, "fletcher_powell": FLETCHER
 STATUS = {0: "CHESSFAD_OK", 1: "CHESSFAD_ERR_ARG", 2: "CHESSFAD_ERR_CHUNK", 3: "CHESSFAD_ERR_FUNC",
           4: "CHESSFAD_ERR_UNSUPPORTED", 5: "CHESSFAD_ERR_CUDA"}
 ALGOS = {"hvp": 0, "hessian": 1, "sym_hvp": 2, "sym_hessian": 3, "hvp_hoisted": 4, "hessian_grad": 5, "hvp_seedsparse": 6,
-         "hessian_seedsparse": 7}
+         "hessian_seedsparse": 7, "sym_hvp_seedsparse": 8, "sym_hessian_seedsparse": 9, "hessian_grad_seedsparse": 10}
 EXPORTS = sorted(["chessfad_hvp_batch", "chessfad_hessian_batch", "chessfad_sym_hvp_batch", "chessfad_sym_hessian_batch",
                   "chessfad_hvp_batch_host", "chessfad_is_supported", "chessfad_is_supported_algo",
                   "chessfad_status_string", "chessfad_model_flops_per_point", "chessfad_model_flops_per_point_algo",
                   "chessfad_fp64_probe", "chessfad_version", "chessfad_hvp_host_workspace_bytes",
                   "chessfad_hvp_batch_hoisted", "chessfad_hvp_batch_seedsparse", "chessfad_hessian_batch_seedsparse", "chessfad_hvp_batch_paper_l2", "chessfad_hessian_grad_batch",
                   "chessfad_hvp_batch_paper", "chessfad_host_ctx_create", "chessfad_host_ctx_destroy",
-                  "chessfad_hvp_batch_host_ctx", "chessfad_path"])
+                  "chessfad_hvp_batch_host_ctx", "chessfad_path", "chessfad_sym_hvp_batch_seedsparse",
+                  "chessfad_sym_hessian_batch_seedsparse", "chessfad_hessian_grad_batch_seedsparse"])
 
 _lock = threading.Lock()
 _lib = None
@@ -58,6 +59,9 @@ def load(build_if_missing: bool = True):
             "chessfad_hvp_batch_hoisted": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_hvp_batch_seedsparse": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_hessian_batch_seedsparse": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
+            "chessfad_sym_hvp_batch_seedsparse": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
+            "chessfad_sym_hessian_batch_seedsparse": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
+            "chessfad_hessian_grad_batch_seedsparse": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_hessian_grad_batch": (i32, [i32, i32, i32, i64, vp, vp, vp, vp, vp]),
             "chessfad_hvp_batch_paper_l2": (i32, [i32, i32, i32, i64, vp, vp, vp, vp]),
             "chessfad_hvp_batch_paper": (i32, [i32, i32, i32, i32, i64, vp, vp, vp, vp]),
@@ -206,25 +210,43 @@ def hessian_batch(func, points, csize: int, params=None, out=None, stream=None):
     return _hess("chessfad_hessian_batch", func, points, csize, params, out, stream)
 
 
-def hessian_grad_batch(func, points, csize: int, params=None, out=None, grad=None, stream=None):
-    """(hess, grad): Alg 5 Hessians plus the gradient by-product from slot v[1] (PAPER.md:252)."""
+def _hess_grad(entry, func, points, csize, params, out, grad, stream):
     import torch
     m, n = _points_2d(points)
     if out is None:
         out = torch.empty((m, n, n), dtype=torch.float64, device=points.device)
     if grad is None:
         grad = torch.empty((m, n), dtype=torch.float64, device=points.device)
-    st = load().chessfad_hessian_grad_batch(_func(func), n, csize, m, _dev(points, "points"),
-                                            _dev(out, "hess", (m, n, n)), _dev(grad, "grad", (m, n)),
-                                            _dev_params(params, func, n), _stream_ptr(stream))
+    st = getattr(load(), entry)(_func(func), n, csize, m, _dev(points, "points"), _dev(out, "hess", (m, n, n)),
+                                _dev(grad, "grad", (m, n)), _dev_params(params, func, n), _stream_ptr(stream))
     _check(st)
     return out, grad
+
+
+def hessian_grad_batch(func, points, csize: int, params=None, out=None, grad=None, stream=None):
+    """(hess, grad): Alg 5 Hessians plus the gradient by-product from slot v[1] (PAPER.md:252)."""
+    return _hess_grad("chessfad_hessian_grad_batch", func, points, csize, params, out, grad, stream)
 
 
 def hessian_batch_seedsparse(func, points, csize: int, params=None, out=None, stream=None):
     """NEXT-4 seed sparsity for the Hessian API (every function): equals hessian_batch bit for
     bit up to the sign of zero."""
     return _hess("chessfad_hessian_batch_seedsparse", func, points, csize, params, out, stream)
+
+
+def sym_hvp_batch_seedsparse(func, points, vecs, csize: int, params=None, out=None, stream=None):
+    """Alg 8 with seed sparsity (F1/F2/F4): equals sym_hvp_batch up to the sign of zero."""
+    return _hvp("chessfad_sym_hvp_batch_seedsparse", func, points, vecs, csize, params, out, stream)
+
+
+def sym_hessian_batch_seedsparse(func, points, csize: int, params=None, out=None, stream=None):
+    """Alg 6 with seed sparsity (F1/F2/F4): equals sym_hessian_batch up to the sign of zero."""
+    return _hess("chessfad_sym_hessian_batch_seedsparse", func, points, csize, params, out, stream)
+
+
+def hessian_grad_batch_seedsparse(func, points, csize: int, params=None, out=None, grad=None, stream=None):
+    """Alg 5 + gradient with seed sparsity (F1/F2/F4): equals hessian_grad_batch."""
+    return _hess_grad("chessfad_hessian_grad_batch_seedsparse", func, points, csize, params, out, grad, stream)
 
 
 def sym_hessian_batch(func, points, csize: int, params=None, out=None, stream=None):

@@ -104,12 +104,19 @@ cudaError_t dispatch_sparse_reg(int func, int Capi, const BatchArgs& a, cudaStre
 #define CHF_SP_CB_SMEM 8  // ... with (A, B) in shared memory (n <= 32): 3 CTAs/SM (measured)
 #endif
 
-template <bool HESS>
+// seed-sparse entry: MODE_HVP / MODE_HESS for every function; the symmetric modes and the
+// gradient for the register functions (F3's seed-sparse kernel implements Alg 7 / Alg 5 only)
+template <int MODE>
 int sparse_entry(int func, int n, int csize, int64_t m, const double* points, const double* vecs, double* out,
-                 const double* params, void* stream) {
+                 const double* params, void* stream, double* grad = nullptr) {
+  constexpr bool HESS = mode_hess(MODE);
   int st = validate(func, n, csize, m, false, params, points, HESS ? out : vecs, out);
   if (st) return st;
+  if (MODE == MODE_HESS_GRAD && m > 0 && !grad) return CHESSFAD_ERR_ARG;
   if (!sparse_supported(func, n)) return CHESSFAD_ERR_UNSUPPORTED;
+  if (func == CHESSFAD_FLETCHER_POWELL && MODE != MODE_HVP && MODE != MODE_HESS) return CHESSFAD_ERR_UNSUPPORTED;
+  if (mode_sym(MODE) && func != CHESSFAD_FLETCHER_POWELL && !supported(func, n, csize, MODE))
+    return CHESSFAD_ERR_UNSUPPORTED;
   if (m == 0) return CHESSFAD_OK;
   BatchArgs a{};
   a.n = n;
@@ -120,8 +127,9 @@ int sparse_entry(int func, int n, int csize, int64_t m, const double* points, co
   a.vecs = vecs;
   a.out = out;
   a.params = params;
+  a.grad = grad;
   if (func != CHESSFAD_FLETCHER_POWELL) {
-    const cudaError_t er = dispatch_sparse_reg<HESS ? MODE_HESS : MODE_HVP>(func, csize, a, (cudaStream_t)stream);
+    const cudaError_t er = dispatch_sparse_reg<MODE>(func, csize, a, (cudaStream_t)stream);
     return er == cudaSuccess ? CHESSFAD_OK : CHESSFAD_ERR_CUDA;
   }
   cudaError_t e = cudaErrorInvalidValue;
@@ -130,7 +138,7 @@ int sparse_entry(int func, int n, int csize, int64_t m, const double* points, co
   while (n % cb) cb >>= 1;
   switch (cb) {
 #define CHF_CASE_SP(CB) \
-  case CB: e = launch_f3_sparse<CB, HESS>(a, (cudaStream_t)stream); break;
+  case CB: e = launch_f3_sparse<CB, MODE == MODE_HESS>(a, (cudaStream_t)stream); break;
     CHF_FOR_CB(CHF_CASE_SP)
 #undef CHF_CASE_SP
   }
@@ -308,12 +316,27 @@ int chessfad_hvp_batch_hoisted(int func, int n, int csize, int64_t m, const doub
 
 int chessfad_hvp_batch_seedsparse(int func, int n, int csize, int64_t m, const double* points, const double* vecs,
                                   double* out, const double* params, void* stream) {
-  return sparse_entry<false>(func, n, csize, m, points, vecs, out, params, stream);
+  return sparse_entry<MODE_HVP>(func, n, csize, m, points, vecs, out, params, stream);
+}
+
+int chessfad_sym_hvp_batch_seedsparse(int func, int n, int csize, int64_t m, const double* points, const double* vecs,
+                                      double* out, const double* params, void* stream) {
+  return sparse_entry<MODE_SYM_HVP>(func, n, csize, m, points, vecs, out, params, stream);
+}
+
+int chessfad_sym_hessian_batch_seedsparse(int func, int n, int csize, int64_t m, const double* points, double* hess,
+                                          const double* params, void* stream) {
+  return sparse_entry<MODE_SYM_HESS>(func, n, csize, m, points, nullptr, hess, params, stream);
+}
+
+int chessfad_hessian_grad_batch_seedsparse(int func, int n, int csize, int64_t m, const double* points, double* hess,
+                                           double* grad, const double* params, void* stream) {
+  return sparse_entry<MODE_HESS_GRAD>(func, n, csize, m, points, nullptr, hess, params, stream, grad);
 }
 
 int chessfad_hessian_batch_seedsparse(int func, int n, int csize, int64_t m, const double* points, double* hess,
                                       const double* params, void* stream) {
-  return sparse_entry<true>(func, n, csize, m, points, nullptr, hess, params, stream);
+  return sparse_entry<MODE_HESS>(func, n, csize, m, points, nullptr, hess, params, stream);
 }
 
 namespace {
@@ -485,11 +508,16 @@ int chessfad_is_supported(int func, int n, int csize) {
 }
 
 int chessfad_is_supported_algo(int func, int n, int csize, int algo) {
-  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_HESSIAN_SEEDSPARSE) return 0;
+  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_HESSIAN_GRAD_SEEDSPARSE) return 0;
   if (validate(func, n, csize, 0, false, func == CHESSFAD_FLETCHER_POWELL ? (const void*)1 : nullptr, nullptr,
                nullptr, nullptr))
     return 0;
   if (algo == CHESSFAD_ALGO_HVP_SEEDSPARSE || algo == CHESSFAD_ALGO_HESSIAN_SEEDSPARSE) return sparse_supported(func, n);
+  if (algo >= CHESSFAD_ALGO_SYM_HVP_SEEDSPARSE) {  // register functions only
+    static const int smode[3] = {MODE_SYM_HVP, MODE_SYM_HESS, MODE_HESS_GRAD};
+    return func != CHESSFAD_FLETCHER_POWELL && sparse_supported(func, n) &&
+           supported(func, n, csize, smode[algo - CHESSFAD_ALGO_SYM_HVP_SEEDSPARSE]);
+  }
   static const int mode_of[6] = {MODE_HVP, MODE_HESS, MODE_SYM_HVP, MODE_SYM_HESS, MODE_HVP_ROWHOIST, MODE_HESS_GRAD};
   return supported(func, n, csize, mode_of[algo]);
 }
@@ -507,7 +535,7 @@ const char* chessfad_status_string(int status) {
 }
 
 double chessfad_model_flops_per_point_algo(int func, int n, int csize, int algo) {
-  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_HESSIAN_SEEDSPARSE) return -1.0;
+  if (algo < CHESSFAD_ALGO_HVP || algo > CHESSFAD_ALGO_HESSIAN_GRAD_SEEDSPARSE) return -1.0;
   if (validate(func, n, csize, 0, false, (const void*)1, nullptr, nullptr, nullptr)) return -1.0;
   const double C = csize, N = n;
   // per-evaluation hDual op counts of the canonical forms (DESIGN.md op table)
@@ -519,11 +547,12 @@ double chessfad_model_flops_per_point_algo(int func, int n, int csize, int algo)
     case CHESSFAD_PRODSUM: hm = N - 1; ha = N - 2; break;
   }
   const double per_eval = hm * (10 * C + 4) + ha * (2 * C + 2) + sm * (2 * C + 2) + sa + un * (4 * C + 2);
-  const bool sym = algo == CHESSFAD_ALGO_SYM_HVP || algo == CHESSFAD_ALGO_SYM_HESSIAN;
+  const bool sym = algo == CHESSFAD_ALGO_SYM_HVP || algo == CHESSFAD_ALGO_SYM_HESSIAN ||
+                   algo == CHESSFAD_ALGO_SYM_HVP_SEEDSPARSE || algo == CHESSFAD_ALGO_SYM_HESSIAN_SEEDSPARSE;
   const double evals = sym ? N * (N / C + 1) / 2 : N * N / C;
   // HVP dot: every H_ij v_j term once (Alg 8: n(n+C)/2 direct + n(n-C)/2 mirrored) = 2n^2
   const bool hvp = algo == CHESSFAD_ALGO_HVP || algo == CHESSFAD_ALGO_SYM_HVP || algo == CHESSFAD_ALGO_HVP_HOISTED ||
-                   algo == CHESSFAD_ALGO_HVP_SEEDSPARSE;
+                   algo == CHESSFAD_ALGO_HVP_SEEDSPARSE || algo == CHESSFAD_ALGO_SYM_HVP_SEEDSPARSE;
   return evals * per_eval + (hvp ? 2 * N * N : 0.0);
 }
 
@@ -539,7 +568,7 @@ int chessfad_fp64_probe(int blocks, int64_t iters, double* sink, void* stream) {
 
 const char* chessfad_path(int func, int n, int csize, int algo) {
   if (!chessfad_is_supported_algo(func, n, csize, algo)) return "unsupported";
-  const bool sparse = algo == CHESSFAD_ALGO_HVP_SEEDSPARSE || algo == CHESSFAD_ALGO_HESSIAN_SEEDSPARSE;
+  const bool sparse = algo >= CHESSFAD_ALGO_HVP_SEEDSPARSE;
   if (func == CHESSFAD_FLETCHER_POWELL) {
     if (sparse) return "f3_seedsparse";
     return "f3_dmma";

@@ -119,8 +119,10 @@ template <int FUNC, int C, int MODE>
 cudaError_t launch_sparse_reg(BatchArgs a, cudaStream_t s) {
   return launch_functor<SparseFunc<FUNC>, C, MODE>(SparseFunc<FUNC>{}, a, s);
 }
-#define CHF_DECL_SPR1(F, C) extern template cudaError_t launch_sparse_reg<F, C, MODE_HVP>(BatchArgs, cudaStream_t); \
-  extern template cudaError_t launch_sparse_reg<F, C, MODE_HESS>(BatchArgs, cudaStream_t);
+#define CHF_FOR_SP_MODE(X, F, C) X(F, C, MODE_HVP) X(F, C, MODE_HESS) X(F, C, MODE_SYM_HVP) X(F, C, MODE_SYM_HESS) \
+  X(F, C, MODE_HESS_GRAD)
+#define CHF_DECL_SPR2(F, C, M) extern template cudaError_t launch_sparse_reg<F, C, M>(BatchArgs, cudaStream_t);
+#define CHF_DECL_SPR1(F, C) CHF_FOR_SP_MODE(CHF_DECL_SPR2, F, C)
 CHF_FOR_C(CHF_DECL_SPR1, FUNC_ROSENBROCK)
 CHF_FOR_C(CHF_DECL_SPR1, FUNC_ACKLEY)
 CHF_FOR_C(CHF_DECL_SPR1, FUNC_PRODSUM)

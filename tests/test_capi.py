@@ -230,3 +230,17 @@ def test_device_header_self_contained(tmp_path):
     r = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-std=c++17", "-O1", "-I", str(inc),
                         "-c", str(src), "-o", str(tmp_path / "user.o")], capture_output=True, text=True, cwd=tmp_path)
     assert r.returncode == 0, r.stderr[-3000:]
+
+
+def test_seedsparse_symmetric_contract(lib):
+    """Seed-sparse Alg 8 / Alg 6 / gradient: register functions only; model = the algorithm's."""
+    import paper_2410_22575_b200 as chf
+    for algo in ("sym_hvp_seedsparse", "sym_hessian_seedsparse", "hessian_grad_seedsparse"):
+        assert chf.is_supported("rosenbrock", 16, 4, algo)
+        assert not chf.is_supported("fletcher_powell", 16, 4, algo)
+        assert chf.path("ackley", 16, 4, algo) == "reg_seedsparse"
+    assert chf.model_flops_per_point("rosenbrock", 16, 4, algo="sym_hvp_seedsparse") == \
+        chf.model_flops_per_point("rosenbrock", 16, 4, algo="sym_hvp")
+    vp = ctypes.c_void_p
+    assert lib.chessfad_hessian_grad_batch_seedsparse(0, 16, 4, 10, vp(1), vp(1), None, None, None) == 1
+    assert lib.chessfad_sym_hvp_batch_seedsparse(2, 16, 4, 10, vp(1), vp(1), vp(1), vp(1), None) == 4

@@ -311,6 +311,42 @@ def test_f3_dmma_all_modes(chf, n, m):
         assert (np.abs(grad.cpu().numpy()[hs[:2]] - g_ref) / gs).max() <= TIGHT
 
 
+@pytest.mark.parametrize("func", ["rosenbrock", "ackley", "prodsum"])
+@pytest.mark.parametrize("n,m", [(6, 90), (16, 200), (64, 40)])
+def test_seedsparse_sym_and_grad(chf, func, n, m):
+    """Seed sparsity for Alg 8, Alg 6 and the gradient by-product (F1/F2/F4): the same values as
+    the per-evaluation symmetric / gradient kernels (up to the sign of zero), and the oracle's
+    Alg 8 / Hessian / gradient; Fletcher-Powell is refused (ERR_UNSUPPORTED)."""
+    P, V = synth.points(45, n, m), synth.vectors(45, n, m)
+    dev = torch.device("cuda")
+    p, v = torch.from_numpy(P).to(dev), torch.from_numpy(V).to(dev)
+    ref7, sabs = oracle.hvp_batch(func, P, V, 1)
+    for C in sorted({1, 2, n // 2 if n // 2 <= 16 else 16}):
+        if n % C or not chf.is_supported(func, n, C, "sym_hvp_seedsparse"):
+            continue
+        a = chf.sym_hvp_batch(func, p, v, C).cpu().numpy()
+        b = chf.sym_hvp_batch_seedsparse(func, p, v, C).cpu().numpy()
+        assert np.array_equal(a, b), C
+        _check(b, oracle.sc_hvp_batch(func, P, V, C), sabs)
+        _check(b, ref7, sabs)
+        Ha = chf.sym_hessian_batch(func, p[:24], C).cpu().numpy()
+        Hb = chf.sym_hessian_batch_seedsparse(func, p[:24], C).cpu().numpy()
+        assert np.array_equal(Ha, Hb), C
+        Ga, ga = chf.hessian_grad_batch(func, p[:24], C)
+        Gb, gb = chf.hessian_grad_batch_seedsparse(func, p[:24], C)
+        assert torch.equal(Ga, Gb) and torch.equal(ga, gb), C
+        href = oracle.hessian_batch(func, P[:24], C)
+        rel = np.abs(Hb - href).max(axis=(1, 2)) / np.abs(href).max(axis=(1, 2))
+        assert rel.max() <= TIGHT
+        g_ref = np.stack([oracle.hessian(func, P[e], None, algo="chunk", C=C)[1] for e in range(4)])
+        gs = np.abs(g_ref).max(axis=1, keepdims=True)
+        assert (np.abs(gb.cpu().numpy()[:4] - g_ref) / gs).max() <= TIGHT
+    pr = torch.from_numpy(synth.fp_params_flat(0, n)).to(dev)
+    assert not chf.is_supported("fletcher_powell", n, 1, "sym_hvp_seedsparse")
+    with pytest.raises(chf.ChessfadError):
+        chf.sym_hvp_batch_seedsparse("fletcher_powell", p, v, 1, pr)
+
+
 @pytest.mark.parametrize("func", ["rosenbrock", "prodsum"])
 def test_sym_hvp_integer_bitwise(chf, func):
     n, m = 16, 200
