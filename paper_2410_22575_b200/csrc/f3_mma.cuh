@@ -36,6 +36,8 @@
 // n = 128): the k range is processed in blocks of KB rows, each evaluation's sums over k split
 // into per-block partial sums that are added into the outputs (global read-add-write by the
 // owning lane; the work per evaluation is unchanged, only the association of the k sum).
+// Alg 8's scatter targets out[e][s] live in a shared-memory tile up to n = 64 and in the
+// output rows themselves beyond (zeroed first; only the owning lane ever touches a row).
 // The sum over k of each second-order entry is a per-lane partial over the k-tiles plus a
 // 3-step butterfly over g; every other reduction order is as in the SIMT kernel.
 #pragma once
@@ -57,9 +59,11 @@ constexpr int f3_mma_kb(int NN) {  // k rows of M per block: all of M up to n = 
 }
 template <int NN, int MODE>
 struct F3Mma {
-  // 8 warps (64 points) whenever M's block and the 64 points' sin/cos tables fit: every n and
-  // mode except the symmetric HVP at n > 64, whose scatter tile needs the room (4 warps)
-  static constexpr int W = (NN <= 64 || MODE != MODE_SYM_HVP) ? 8 : 4;
+  static constexpr int W = 8;
+  // Alg 8's scatter targets: a shared-memory tile up to n = 64; beyond, the output rows
+  // themselves in global memory (the tile would not fit next to M's block and the tables)
+  static constexpr bool kSmemScatter = MODE == MODE_SYM_HVP && NN <= 64;
+  static constexpr bool kGlobalScatter = MODE == MODE_SYM_HVP && NN > 64;
   static constexpr int KB = f3_mma_kb(NN);
   static constexpr int P = W * kMmaPPW;        // points per CTA
   static constexpr int TS = P + 8;             // sin/cos table row stride (doubles): 2 wavefronts per LDS
@@ -68,7 +72,7 @@ struct F3Mma {
   static constexpr size_t kMf = (size_t)2 * KB * NN;  // one M block in fragment order
   static constexpr size_t kTab = (size_t)NN * TS;
   static constexpr size_t smem_bytes() {
-    return (kMf + NN + 2 * kTab + (MODE == MODE_SYM_HVP ? (size_t)P * (NN + 1) : 0)) * sizeof(double);
+    return (kMf + NN + 2 * kTab + (kSmemScatter ? (size_t)P * (NN + 1) : 0)) * sizeof(double);
   }
   static_assert(NN % 8 == 0 && NN % KB == 0 && KB % 8 == 0, "tile shapes");
 };
@@ -83,7 +87,7 @@ __global__ void __launch_bounds__(F3Mma<NN, MODE>::W * 32, 1) hvp_f3_mma_kernel(
   double* Es = Mf + Cfg::kMf;        // [NN]            E*, zero-padded
   double* s_tab = Es + NN;           // [NN][TS]        sin a_j of the CTA's points, zero-padded
   double* c_tab = s_tab + Cfg::kTab; // [NN][TS]        cos a_j
-  double* s_acc = c_tab + Cfg::kTab; // [P][NN+1]       MODE_SYM_HVP scatter targets
+  double* s_acc = c_tab + Cfg::kTab; // [P][NN+1]       MODE_SYM_HVP scatter targets (n <= 64)
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int n = p.n;
   const int64_t e0 = (int64_t)blockIdx.x * P;
@@ -101,7 +105,7 @@ __global__ void __launch_bounds__(F3Mma<NN, MODE>::W * 32, 1) hvp_f3_mma_kernel(
     s_tab[j * TS + pt] = sv;
     c_tab[j * TS + pt] = cv;
   }
-  if (MODE == MODE_SYM_HVP)
+  if (Cfg::kSmemScatter)
     for (int q = tid; q < P * (NN + 1); q += nthr) s_acc[q] = 0.0;
 
   const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -126,6 +130,12 @@ __global__ void __launch_bounds__(F3Mma<NN, MODE>::W * 32, 1) hvp_f3_mma_kernel(
   };
   // k-blocked outputs: the first block stores, later blocks add their partial sums
   auto emit = [&](double* dst, double v, bool first) { *dst = first ? v : *dst + v; };
+
+  if (Cfg::kGlobalScatter && g == 0)  // every contribution to out is added (scatter + rows)
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+      if (eD[h] < p.m)
+        for (int i = 0; i < n; i++) p.out[eD[h] * n + i] = 0.0;
 
   for (int kb0 = 0; kb0 < NN; kb0 += KB) {
     const bool first = kb0 == 0;
@@ -247,8 +257,13 @@ __global__ void __launch_bounds__(F3Mma<NN, MODE>::W * 32, 1) hvp_f3_mma_kernel(
             if (MODE == MODE_HVP || MODE == MODE_HVP_ROWHOIST || MODE == MODE_SYM_HVP) {
               res[h] = res[h] + fC[h] * __ldg(p.vecs + eDc[h] * n + col);  // Alg 7 :392-394
               if (MODE == MODE_SYM_HVP && mirror && g == 0) {                 // Alg 8 scatter
-                double* acc = s_acc + (warp * kMmaPPW + 2 * t + h) * (NN + 1) + col;
-                *acc = *acc + fC[h] * vi[h];
+                if (Cfg::kSmemScatter) {
+                  double* acc = s_acc + (warp * kMmaPPW + 2 * t + h) * (NN + 1) + col;
+                  *acc = *acc + fC[h] * vi[h];
+                } else if (eD[h] < p.m) {  // the owning lane's own output row (zeroed below)
+                  double* acc = p.out + eD[h] * n + col;
+                  *acc = *acc + fC[h] * vi[h];
+                }
               }
             } else if (g == 0 && eD[h] < p.m) {
               emit(p.out + (eD[h] * n + i) * n + col, fC[h], first);       // Alg 5 :210-212
@@ -260,10 +275,10 @@ __global__ void __launch_bounds__(F3Mma<NN, MODE>::W * 32, 1) hvp_f3_mma_kernel(
       if (!HESS && g == 0)
 #pragma unroll
         for (int h = 0; h < 2; h++)
-          if (eD[h] < p.m) emit(p.out + eD[h] * n + i, res[h], first);
+          if (eD[h] < p.m) emit(p.out + eD[h] * n + i, res[h], first && !Cfg::kGlobalScatter);
     }
   }
-  if (MODE == MODE_SYM_HVP) {  // Alg 8: add the scattered mirror terms H_is v_i (all k blocks)
+  if (Cfg::kSmemScatter) {  // Alg 8: add the scattered mirror terms H_is v_i
     __syncthreads();
     for (int q = tid; q < P * n; q += nthr) {
       const int pt = q / n, i = q - pt * n;
