@@ -237,6 +237,7 @@ def main(argv=None):
     if rc is not None:
         return rc
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    args.device_index = local
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -444,7 +445,7 @@ def main(argv=None):
             with open(args.sweep_out, "w") as f:
                 json.dump({"headline": line, "sweep": sweep, "paper_l2_baseline": paper_l2, "small_n_hbm": small_hbm},
                           f, indent=1)
-        print(json.dumps(_round(line), separators=(",", ":")), flush=True)
+        print(compact_line(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -464,7 +465,9 @@ def run_sweep(chf, args, pts, vec, out, params, stream, m, m_all, peak_tf, per_s
                 if n % c or not chf.is_supported(f, n, c, algo):
                     continue
                 ks = 10
-                tt, per = timed_steps(lambda: fnb(f, pts, vec, c, params[f], out=out), ks, 3)
+                cs_ = ClockSampler(args.device_index)
+                tt, per = timed_steps(lambda: fnb(f, pts, vec, c, params[f], out=out), ks, 3, cs_)
+                clk = cs_.summary()
                 tt = max_over_ranks(tt) / ks
                 fl = chf.model_flops_per_point(f, n, c, algo=algo)
                 exs = executed_entry(f, n, c, src_hash, algo)
@@ -472,7 +475,8 @@ def run_sweep(chf, args, pts, vec, out, params, stream, m, m_all, peak_tf, per_s
                 sweep.append({"algo": algo, "func": f, "csize": c, "hvp_per_s": m_all / tt, "ms": tt * 1e3,
                               "ms_median": float(np.median(per)) * 1e3, "ms_best": min(per) * 1e3,
                               "model_tflops_effective": m * fl / tt / 1e12, "executed_tflops": ex_tf,
-                              "executed_frac": None if ex_tf is None else ex_tf / peak_tf})
+                              "executed_frac": None if ex_tf is None else ex_tf / peak_tf,
+                              "sm_mhz": clk["sm_mhz"], "clock_reasons": clk["reasons"]})
     paper_l2 = None
     if args.func in ("rosenbrock", "prodsum") and n in (2, 4, 8, 16):
         best = None
@@ -550,6 +554,25 @@ def executed_entry(func, n, C, src_hash, algo="hvp", path=None):
         ent["executed_flops_per_point"] = ratio * chf.model_flops_per_point(func, n, C, algo=algo)
         ent["basis"] = f"STALE: executed/model ratio {ratio:.3f} measured by ncu on build {tab.get('src_hash')}"
     return ent
+
+
+LINE_LIMIT = 2000  # the driver keeps the last ~4 KB of stdout; one line must fit well inside
+OPTIONAL_KEYS = (("roofline", "basis"), ("roofline", "peak_basis"), (None, "sweep_file"), (None, "paper_l2_speedup"),
+                 (None, "small_n_hbm_frac"), (None, "sweep_best_hvp"), ("config", "l2"))
+
+
+def compact_line(line: dict, limit: int = LINE_LIMIT) -> str:
+    """The final stdout line: 4-significant-digit floats, compact separators; optional
+    descriptive keys are dropped (in OPTIONAL_KEYS order) until it fits in `limit` bytes."""
+    line = json.loads(json.dumps(line))
+    text = json.dumps(_round(line), separators=(",", ":"))
+    for parent, key in OPTIONAL_KEYS:
+        if len(text) <= limit:
+            break
+        d = line if parent is None else line.get(parent) or {}
+        d.pop(key, None)
+        text = json.dumps(_round(line), separators=(",", ":"))
+    return text
 
 
 def _round(x):

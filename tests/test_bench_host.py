@@ -79,3 +79,37 @@ def test_world_size_mismatch_rejected(monkeypatch):
         bench.maybe_respawn(a, ["--gpus", "2"])
     monkeypatch.setenv("WORLD_SIZE", "2")
     assert bench.maybe_respawn(a, ["--gpus", "2"]) is None
+
+
+def test_compact_line_fits_driver_tail():
+    """The headline line stays < 2 KB even with every optional key at worst-case length; the
+    required keys survive."""
+    import json
+    big = 1.2345678901234567e300
+    line = {"metric": bench.METRIC, "value": big, "unit": "HVP/s", "n_gpus": 8, "steps": 100, "warmup": 5,
+            "ms_per_step": big, "step_ms": {"median": big, "best": big}, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "x" * 80, "func": "fletcher_powell", "n": 128, "csize": 128, "m_per_gpu": 1 << 20,
+                       "global_points": 8 << 20, "seed": 0, "parallelism": "dp8", "l2": "y" * 60},
+            "roofline": {k: big for k in ("achieved", "peak", "frac", "frac_executed", "frac_model",
+                                          "executed_over_model", "model_flops_per_point", "traffic",
+                                          "algorithmic_bytes", "hbm_gbs", "fp64_pipe_pct_ncu", "fp64_probe_tflops")},
+            "cpu_baseline": {"value": big, "unit": "HVP/s", "cores": 64, "kind": "oracle", "sample": "z" * 120},
+            "e2e": {"value": big, "unit": "HVP/s", "h2d_bytes_per_step": 1 << 40, "d2h_bytes_per_step": 1 << 40,
+                    "ms_per_step": big, "api": "chessfad_hvp_batch_host_ctx"},
+            "gpu_launches": 100, "clocks": {"sm_mhz": 1965.0, "sm_max_mhz": 1965, "reasons": ["sw_power_cap"] * 3,
+                                            "samples": 99},
+            "parity": {"max_err": big, "points": 1 << 20, "of": 1 << 20, "bar": 1e-10, "pass": True},
+            "strong": {"workload": "cfg5 m=8388608", "value": big, "ms": big, "value_with_gather": big,
+                       "ms_with_gather": big, "gather": "all_gather_into_tensor in place", "gather_parity": True},
+            "sweep_best_hvp": {f: [16, big] for f in ("rosenbrock", "ackley", "fletcher_powell", "prodsum")},
+            "small_n_hbm_frac": {f"f{i}": big for i in range(4)}, "paper_l2_speedup": big,
+            "sweep_file": "gpurun_out/bench_sweep.json"}
+    line["roofline"].update({"bound": "alu", "unit": "TFLOP/s", "basis": "b" * 120, "peak_basis": "p" * 40})
+    text = bench.compact_line(line)
+    assert len(text) < 2048
+    d = json.loads(text)
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "roofline", "cpu_baseline",
+              "e2e", "gpu_launches", "clocks", "parity", "config"):
+        assert k in d
+    assert d["roofline"]["frac"] == float(f"{big:.4g}")

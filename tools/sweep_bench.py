@@ -19,7 +19,7 @@ import torch  # noqa: E402
 
 import paper_2410_22575_b200 as chf  # noqa: E402
 import synth  # noqa: E402
-from bench import executed_entry  # noqa: E402
+from bench import ClockSampler, executed_entry  # noqa: E402
 from paper_2410_22575_b200.build import source_hash  # noqa: E402
 
 PEAK = 148 * 64 * 2 * 1.965e9 / 1e12
@@ -59,12 +59,15 @@ def main():
             one = time.perf_counter() - t0
             reps = max(1, min(50, int(args.min_seconds / max(one, 1e-6))))
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(reps):
-                call()
-            e1.record()
-            torch.cuda.synchronize()
+            clk = ClockSampler(0)
+            with clk:
+                e0.record()
+                for _ in range(reps):
+                    call()
+                e1.record()
+                torch.cuda.synchronize()
             t = e0.elapsed_time(e1) / 1e3 / reps
+            clocks = clk.summary()
             mf = chf.model_flops_per_point(f, n, c, algo=args.algo)
             ex = executed_entry(f, n, c, source_hash(), args.algo)  # valid by kernel SASS hash (bench.py)
             if ex is not None and ex["basis"].startswith("STALE"):
@@ -73,6 +76,7 @@ def main():
                    "model_flops_per_point": mf, "model_tflops_effective": m * mf / t / 1e12,
                    "executed_tflops": None if ex is None else m * ex["executed_flops_per_point"] / t / 1e12}
             rec["executed_frac"] = None if ex is None else rec["executed_tflops"] / PEAK
+            rec["sm_mhz"], rec["clock_reasons"] = clocks["sm_mhz"], clocks["reasons"]
             print(json.dumps(rec), flush=True)
         del pts, vec, out
         torch.cuda.empty_cache()
