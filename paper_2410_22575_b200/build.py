@@ -101,6 +101,12 @@ def _build_locked(jobs, defines, out) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
     os.replace(tmp, target)
+    try:  # per-kernel SASS fingerprints, cached next to the library (sass.py)
+        from . import sass as _sass
+    except ImportError:
+        import sass as _sass  # run as a script
+    _sass.kernel_sass_hashes.cache_clear()
+    _sass.kernel_sass_hashes(target)
     return target
 
 

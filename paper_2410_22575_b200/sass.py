@@ -18,10 +18,47 @@ def _tool(name: str) -> str | None:
     return shutil.which(name) or (f"/usr/local/cuda/bin/{name}" if name == "cuobjdump" else None)
 
 
+def _file_digest(path: str) -> str:
+    h = hashlib.sha256()
+    with open(path, "rb") as f:
+        for blk in iter(lambda: f.read(1 << 22), b""):
+            h.update(blk)
+    return h.hexdigest()[:16]
+
+
 @functools.lru_cache(maxsize=4)
 def kernel_sass_hashes(lib_path: str) -> dict:
     """{demangled kernel name: sha256(SASS instruction text)[:16]} for every kernel in
-    lib_path ({} if the tools are unavailable)."""
+    lib_path ({} if the tools are unavailable).  Disassembling the library takes ~30 s, so the
+    table is cached next to it (<lib>.sass.json, written at build time) and reused while the
+    library's own sha256 matches."""
+    import json
+    import os
+    cache = lib_path + ".sass.json"
+    try:
+        digest = _file_digest(lib_path)
+    except OSError:
+        return {}
+    try:
+        with open(cache) as f:
+            d = json.load(f)
+        if d.get("lib_sha256") == digest:
+            return d["hashes"]
+    except (OSError, ValueError, KeyError):
+        pass
+    hashes = _disassemble_hashes(lib_path)
+    if hashes:
+        try:
+            tmp = cache + f".tmp{os.getpid()}"
+            with open(tmp, "w") as f:
+                json.dump({"lib_sha256": digest, "hashes": hashes}, f)
+            os.replace(tmp, cache)
+        except OSError:
+            pass
+    return hashes
+
+
+def _disassemble_hashes(lib_path: str) -> dict:
     cuobjdump, cxxfilt = _tool("cuobjdump"), _tool("c++filt")
     if not cuobjdump or not cxxfilt:
         return {}
