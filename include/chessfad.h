@@ -147,13 +147,16 @@ int chessfad_hessian_batch_seedsparse(int func, int n, int csize, int64_t m, con
 
 /*
  * Seed sparsity (as chessfad_hvp_batch_seedsparse) for the symmetric algorithms and the
- * gradient by-product, Rosenbrock / Ackley / prodsum: Alg 8 SC-HESS-VEC,
+ * gradient by-product: Alg 8 SC-HESS-VEC,
  * Alg 6 SCHUNK-HESS and Alg 5 + gradient, evaluating only the
  * terms of each running sum that touch row i or the chunk (the others add exact +-0 to every
  * derivative slot; the gradient slot v[1] needs only the terms touching i).  Arguments,
  * layouts and results as chessfad_sym_hvp_batch / chessfad_sym_hessian_batch /
- * chessfad_hessian_grad_batch (bit-identical up to the sign of zero); executed FLOPs below the
- * model.  Fletcher-Powell: ERR_UNSUPPORTED (its seed-sparse kernel implements Alg 7 / Alg 5).
+ * chessfad_hessian_grad_batch (bit-identical up to the sign of zero; Fletcher-Powell: within
+ * rounding of its tensor-core per-evaluation kernel); executed FLOPs below the model.
+ * Fletcher-Powell: Alg 6 and the gradient are supported (each (i, col) entry O(n); Alg 6 skips
+ * the column blocks below row i's chunk for n <= 32 or n % 8 != 0, and mirrors); Alg 8 is
+ * ERR_UNSUPPORTED (its scatter crosses the warps that own a point's rows in that kernel).
  */
 int chessfad_sym_hvp_batch_seedsparse(int func, int n, int csize, int64_t m, const double *points,
                                       const double *vecs, double *out, const double *params, void *stream);
@@ -236,8 +239,8 @@ enum chessfad_algo {
   CHESSFAD_ALGO_HVP_SEEDSPARSE = 6, /* Alg 7 + NEXT-4 seed sparsity, chessfad_hvp_batch_seedsparse */
   CHESSFAD_ALGO_HESSIAN_SEEDSPARSE = 7, /* Alg 5 + seed sparsity, chessfad_hessian_batch_seedsparse */
   CHESSFAD_ALGO_SYM_HVP_SEEDSPARSE = 8, /* Alg 8 + seed sparsity (F1/F2/F4), chessfad_sym_hvp_batch_seedsparse */
-  CHESSFAD_ALGO_SYM_HESSIAN_SEEDSPARSE = 9, /* Alg 6 + seed sparsity (F1/F2/F4), chessfad_sym_hessian_batch_seedsparse */
-  CHESSFAD_ALGO_HESSIAN_GRAD_SEEDSPARSE = 10 /* Alg 5 + gradient + seed sparsity (F1/F2/F4) */
+  CHESSFAD_ALGO_SYM_HESSIAN_SEEDSPARSE = 9, /* Alg 6 + seed sparsity, chessfad_sym_hessian_batch_seedsparse */
+  CHESSFAD_ALGO_HESSIAN_GRAD_SEEDSPARSE = 10 /* Alg 5 + gradient + seed sparsity */
 };
 
 /* 1 if (func, n, csize) runs for the given algorithm, else 0. */

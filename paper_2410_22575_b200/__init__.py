@@ -240,12 +240,14 @@ def sym_hvp_batch_seedsparse(func, points, vecs, csize: int, params=None, out=No
 
 
 def sym_hessian_batch_seedsparse(func, points, csize: int, params=None, out=None, stream=None):
-    """Alg 6 with seed sparsity (F1/F2/F4): equals sym_hessian_batch up to the sign of zero."""
+    """Alg 6 with seed sparsity (every function): equals sym_hessian_batch up to the sign of zero
+    (Fletcher-Powell: within rounding)."""
     return _hess("chessfad_sym_hessian_batch_seedsparse", func, points, csize, params, out, stream)
 
 
 def hessian_grad_batch_seedsparse(func, points, csize: int, params=None, out=None, grad=None, stream=None):
-    """Alg 5 + gradient with seed sparsity (F1/F2/F4): equals hessian_grad_batch."""
+    """Alg 5 + gradient with seed sparsity (every function): equals hessian_grad_batch
+    (Fletcher-Powell: within rounding)."""
     return _hess_grad("chessfad_hessian_grad_batch_seedsparse", func, points, csize, params, out, grad, stream)
 
 

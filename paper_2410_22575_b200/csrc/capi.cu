@@ -114,7 +114,7 @@ int sparse_entry(int func, int n, int csize, int64_t m, const double* points, co
   if (st) return st;
   if (MODE == MODE_HESS_GRAD && m > 0 && !grad) return CHESSFAD_ERR_ARG;
   if (!sparse_supported(func, n)) return CHESSFAD_ERR_UNSUPPORTED;
-  if (func == CHESSFAD_FLETCHER_POWELL && MODE != MODE_HVP && MODE != MODE_HESS) return CHESSFAD_ERR_UNSUPPORTED;
+  if (func == CHESSFAD_FLETCHER_POWELL && MODE == MODE_SYM_HVP) return CHESSFAD_ERR_UNSUPPORTED;
   if (mode_sym(MODE) && func != CHESSFAD_FLETCHER_POWELL && !supported(func, n, csize, MODE))
     return CHESSFAD_ERR_UNSUPPORTED;
   if (m == 0) return CHESSFAD_OK;
@@ -138,7 +138,7 @@ int sparse_entry(int func, int n, int csize, int64_t m, const double* points, co
   while (n % cb) cb >>= 1;
   switch (cb) {
 #define CHF_CASE_SP(CB) \
-  case CB: e = launch_f3_sparse<CB, MODE == MODE_HESS>(a, (cudaStream_t)stream); break;
+  case CB: e = launch_f3_sparse<CB, MODE>(a, (cudaStream_t)stream); break;
     CHF_FOR_CB(CHF_CASE_SP)
 #undef CHF_CASE_SP
   }
@@ -513,10 +513,10 @@ int chessfad_is_supported_algo(int func, int n, int csize, int algo) {
                nullptr, nullptr))
     return 0;
   if (algo == CHESSFAD_ALGO_HVP_SEEDSPARSE || algo == CHESSFAD_ALGO_HESSIAN_SEEDSPARSE) return sparse_supported(func, n);
-  if (algo >= CHESSFAD_ALGO_SYM_HVP_SEEDSPARSE) {  // register functions only
+  if (algo >= CHESSFAD_ALGO_SYM_HVP_SEEDSPARSE) {  // Fletcher-Powell: no seed-sparse Alg 8
     static const int smode[3] = {MODE_SYM_HVP, MODE_SYM_HESS, MODE_HESS_GRAD};
-    return func != CHESSFAD_FLETCHER_POWELL && sparse_supported(func, n) &&
-           supported(func, n, csize, smode[algo - CHESSFAD_ALGO_SYM_HVP_SEEDSPARSE]);
+    if (func == CHESSFAD_FLETCHER_POWELL) return algo != CHESSFAD_ALGO_SYM_HVP_SEEDSPARSE && sparse_supported(func, n);
+    return sparse_supported(func, n) && supported(func, n, csize, smode[algo - CHESSFAD_ALGO_SYM_HVP_SEEDSPARSE]);
   }
   static const int mode_of[6] = {MODE_HVP, MODE_HESS, MODE_SYM_HVP, MODE_SYM_HESS, MODE_HVP_ROWHOIST, MODE_HESS_GRAD};
   return supported(func, n, csize, mode_of[algo]);

@@ -187,10 +187,11 @@ CHF_INL void f3_sp_block_staged(int n, int i, int cb, bool row0, double si, doub
 
 // row i: out_i = sum_col d2f/dx_i dx_col * v_col, ascending columns (HVP), or the row stored
 // to hrow (HESS; nullptr for ragged-tail lanes)
-template <bool ROW0, class AB>
+template <bool ROW0, bool GRAD, class AB>
 CHF_INL double f3_sp_diag(int n, int i, double si, double ci, const AB& ab,
-                          const double* __restrict__ r0t) {
-  // diagonal column: the full slot set (r0, r1 = r2, rC), f3_phase_b's expression
+                          const double* __restrict__ r0t, double& f1) {
+  // diagonal column: the full slot set (r0, r1 = r2, rC), f3_phase_b's expression; GRAD: also
+  // slot 1 of f = sum_k r_k r_k, df/dx_i = sum_k (r0 r1 + r0 r1) (Fig. 1 product)
   double fdiag = 0.0;
   for (int k = 0; k < n; k++) {
     const double2 c = ab(k, i);
@@ -202,19 +203,33 @@ CHF_INL double f3_sp_diag(int n, int i, double si, double ci, const AB& ab,
     const double rC = ROW0 ? -__fma_rn(c.x, -si, __dmul_rn(c.y, -ci)) : -f3_sp_term<false>(c.x, -si, c.y, -ci);
     const double rrC = r0 * rC + r1 * r2 + r1 * r2 + r0 * rC;
     fdiag = (k == 0) ? rrC : fdiag + rrC;
+    if (GRAD) {
+      const double rr1 = r0 * r1 + r0 * r1;
+      f1 = (k == 0) ? rr1 : f1 + rr1;
+    }
   }
   return fdiag;
 }
 
-// row0 is a runtime flag so that the staged path's barriers are shared by all warps
-template <int CB, bool HESS, bool STAGED, class AB>
-CHF_INL double f3_sp_row(int n, int i, bool row0, const AB& ab, const double* __restrict__ sa,
+// row0 is a runtime flag so that the staged path's barriers are shared by all warps.
+// MODE: MODE_HVP (returns the row of H v), MODE_HESS (stores the row to hrow), MODE_SYM_HESS
+// (Alg 6: stores the entries of chunks >= row i's chunk, mirrors those of later chunks into
+// hcol[col * n]; the unstaged path also skips the column blocks wholly below row i's chunk --
+// the staged path keeps every warp on the same block sequence for its shared barriers),
+// MODE_HESS_GRAD (stores the row and returns df/dx_i through f1).
+template <int CB, int MODE, bool STAGED, class AB>
+CHF_INL double f3_sp_row(int n, int Capi, int i, bool row0, const AB& ab, const double* __restrict__ sa,
                          const double* __restrict__ ca, const double* __restrict__ r0t, const double* __restrict__ v,
-                         int vs, double* __restrict__ hrow, const SpRing& rg) {
+                         int vs, double* __restrict__ hrow, double* __restrict__ hcol, const SpRing& rg, double& f1) {
+  constexpr bool HESS = mode_hess(MODE);
+  constexpr bool GRAD = MODE == MODE_HESS_GRAD;
   const double si = sa[i * kPad], ci = ca[i * kPad];
-  const double fdiag = row0 ? f3_sp_diag<true>(n, i, si, ci, ab, r0t) : f3_sp_diag<false>(n, i, si, ci, ab, r0t);
+  const double fdiag = row0 ? f3_sp_diag<true, GRAD>(n, i, si, ci, ab, r0t, f1)
+                            : f3_sp_diag<false, GRAD>(n, i, si, ci, ab, r0t, f1);
+  const int cs_row = (i / Capi) * Capi;  // first column of row i's chunk (Alg 6)
   double res = 0.0;
-  for (int cb = 0; cb < n; cb += CB) {
+  const int cb_first = (MODE == MODE_SYM_HESS && !STAGED) ? cs_row / CB * CB : 0;
+  for (int cb = cb_first; cb < n; cb += CB) {
     double fC[CB];
     if constexpr (STAGED) {
       f3_sp_block_staged<CB>(n, i, cb, row0, si, ci, ab, rg, sa, ca, fC);
@@ -229,7 +244,15 @@ CHF_INL double f3_sp_row(int n, int i, bool row0, const AB& ab, const double* __
     for (int q = 0; q < CB; q++) {
       const double h = (cb + q == i) ? fdiag : fC[q];
       if (HESS) {
-        if (hrow) hrow[cb + q] = h;  // a7': H[e][i][col] (Alg 5)
+        const int col = cb + q;
+        if (MODE == MODE_SYM_HESS) {
+          if (hrow && col >= cs_row) {
+            hrow[col] = h;                                              // Alg 6 :229-235
+            if (col / Capi > i / Capi) hcol[(size_t)col * n] = h;       // mirror, :237-241 (G9)
+          }
+        } else if (hrow) {
+          hrow[col] = h;  // a7': H[e][i][col] (Alg 5)
+        }
       } else {
         res = __fma_rn(h, v[(cb + q) * vs], res);  // a5/a6: ascending columns, as RowSink
       }
@@ -240,11 +263,12 @@ CHF_INL double f3_sp_row(int n, int i, bool row0, const AB& ab, const double* __
 
 // AB_SMEM (n <= 32): (A, B) whole in shared memory, else the interleaved global scratch.
 // SLIM (n > 32): vectors read and outputs written straight from/to global memory (3 tiles).
-// HESS: the Hessian (Alg 5 output, hess[e][i][j]) instead of the HVP.
+// MODE: MODE_HVP, or a Hessian mode (Alg 5 output hess[e][i][j]; Alg 6; Alg 5 + gradient).
 // STAGED (SLIM, n % kSpKS == 0): the CTA-shared (A, B) block rows go through the cp.async
 // double buffer (f3_sp_block_staged); every warp then has n / 4 rows (uniform barriers).
-template <int CB, bool AB_SMEM, bool SLIM, bool HESS, bool STAGED>
+template <int CB, bool AB_SMEM, bool SLIM, int MODE, bool STAGED>
 __global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? CHF_SP_MINB_SMEM : CHF_SP_MINB) hvp_f3_sparse_kernel(BatchArgs p) {
+  constexpr bool HESS = mode_hess(MODE);
   extern __shared__ double smem[];
   const int n = p.n, G = p.groups, P = 32 * G;
   double* s_sa = smem;                 // [G][n][33]  sin a
@@ -303,7 +327,10 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? CHF_SP_MINB_SMEM : CH
   const SpRing rg{s_ab, s_ab + 2 * kSpKS * CB + warp * 2 * kSpKS};
   for (int i = wg; i < n; i += rstep) {
     double* hrow = (HESS && e < p.m) ? p.out + (e * n + i) * n : nullptr;
-    const double res = f3_sp_row<CB, HESS, STAGED>(n, i, i == 0, ab, sa, ca, r0t, v, vs, hrow, rg);
+    double* hcol = (HESS && e < p.m) ? p.out + e * n * n + i : nullptr;
+    double f1 = 0.0;
+    const double res = f3_sp_row<CB, MODE, STAGED>(n, p.csize, i, i == 0, ab, sa, ca, r0t, v, vs, hrow, hcol, rg, f1);
+    if (MODE == MODE_HESS_GRAD && e < p.m) p.grad[e * n + i] = f1;
     if (HESS) {
     } else if (SLIM) {
       if (e < p.m) p.out[e * n + i] = res;

@@ -3,7 +3,7 @@
 #include "launch.cuh"
 
 namespace chessfad {
-#define CHF_INST_SP(CB) template cudaError_t launch_f3_sparse<CB, false>(BatchArgs, cudaStream_t); \
-  template cudaError_t launch_f3_sparse<CB, true>(BatchArgs, cudaStream_t);
+#define CHF_INST_SP1(CB, M) template cudaError_t launch_f3_sparse<CB, M>(BatchArgs, cudaStream_t);
+#define CHF_INST_SP(CB) CHF_FOR_F3SP_MODE(CHF_INST_SP1, CB)
 CHF_FOR_CB(CHF_INST_SP)
 }  // namespace chessfad

@@ -27,19 +27,20 @@ inline size_t f3_sparse_smem_bytes(int n, int G) {
   return (size_t)tiles * G * n * kPad * sizeof(double) + (f3_ab_smem(n) ? (size_t)n * n * 2 * sizeof(double) : 0) +
          (f3_sp_staged(n) ? ring : 0);
 }
-template <int CB, bool HESS>
+template <int CB, int MODE>
 cudaError_t launch_f3_sparse(BatchArgs a, cudaStream_t s) {
   a.groups = groups_for(a.n, kWarpsF3, MODE_HVP);
   const int64_t P = 32 * a.groups;
   const int grid = (int)((a.m + P - 1) / P);
   const size_t smem = f3_sparse_smem_bytes(a.n, a.groups);
-  if (f3_ab_smem(a.n)) return launch_with_smem(hvp_f3_sparse_kernel<CB, true, false, HESS, false>, grid, kWarpsF3 * 32, smem, s, a);
-  return f3_sp_staged(a.n) ? launch_with_smem(hvp_f3_sparse_kernel<CB, false, true, HESS, true>, grid, kWarpsF3 * 32, smem, s, a)
-                           : launch_with_smem(hvp_f3_sparse_kernel<CB, false, true, HESS, false>, grid, kWarpsF3 * 32, smem, s, a);
+  if (f3_ab_smem(a.n)) return launch_with_smem(hvp_f3_sparse_kernel<CB, true, false, MODE, false>, grid, kWarpsF3 * 32, smem, s, a);
+  return f3_sp_staged(a.n) ? launch_with_smem(hvp_f3_sparse_kernel<CB, false, true, MODE, true>, grid, kWarpsF3 * 32, smem, s, a)
+                           : launch_with_smem(hvp_f3_sparse_kernel<CB, false, true, MODE, false>, grid, kWarpsF3 * 32, smem, s, a);
 }
 #define CHF_FOR_CB(X) X(1) X(2) X(4) X(8) X(16)
-#define CHF_DECL_SP(CB) extern template cudaError_t launch_f3_sparse<CB, false>(BatchArgs, cudaStream_t); \
-  extern template cudaError_t launch_f3_sparse<CB, true>(BatchArgs, cudaStream_t);
+#define CHF_FOR_F3SP_MODE(X, CB) X(CB, MODE_HVP) X(CB, MODE_HESS) X(CB, MODE_SYM_HESS) X(CB, MODE_HESS_GRAD)
+#define CHF_DECL_SP1(CB, M) extern template cudaError_t launch_f3_sparse<CB, M>(BatchArgs, cudaStream_t);
+#define CHF_DECL_SP(CB) CHF_FOR_F3SP_MODE(CHF_DECL_SP1, CB)
 CHF_FOR_CB(CHF_DECL_SP)
 
 // hoisted HVP (NEXT-4) for n = NS in {2, 4, 8, 16}: thread per point, compile-time seeds

@@ -233,11 +233,12 @@ def test_device_header_self_contained(tmp_path):
 
 
 def test_seedsparse_symmetric_contract(lib):
-    """Seed-sparse Alg 8 / Alg 6 / gradient: register functions only; model = the algorithm's."""
+    """Seed-sparse Alg 8 / Alg 6 / gradient: every function except Alg 8 for Fletcher-Powell;
+    model = the algorithm's."""
     import paper_2410_22575_b200 as chf
     for algo in ("sym_hvp_seedsparse", "sym_hessian_seedsparse", "hessian_grad_seedsparse"):
         assert chf.is_supported("rosenbrock", 16, 4, algo)
-        assert not chf.is_supported("fletcher_powell", 16, 4, algo)
+        assert chf.is_supported("fletcher_powell", 16, 4, algo) == (algo != "sym_hvp_seedsparse")
         assert chf.path("ackley", 16, 4, algo) == "reg_seedsparse"
     assert chf.model_flops_per_point("rosenbrock", 16, 4, algo="sym_hvp_seedsparse") == \
         chf.model_flops_per_point("rosenbrock", 16, 4, algo="sym_hvp")

@@ -431,6 +431,36 @@ def _same_as_per_eval(chf, n, C, a, b, algo="hvp"):
     assert (np.abs(a - b) / scale).max() <= TIGHT, f"C={C}: max rel diff {(np.abs(a - b) / scale).max():.3e}"
 
 
+@pytest.mark.parametrize("n,m", [(6, 70), (16, 130), (40, 20), (64, 9)])
+def test_seedsparse_f3_sym_hessian_and_grad(chf, n, m):
+    """F3 seed sparsity for Alg 6 (upper chunks computed, later chunks mirrored) and the
+    gradient by-product, against the per-evaluation (tensor-core) Hessian / gradient and the
+    oracle; n = 40 and 64 take the unstaged / staged (A, B) paths."""
+    func = "fletcher_powell"
+    P = synth.points(22, n, m)
+    params = synth.fp_params_flat(0, n)
+    dev = torch.device("cuda")
+    p, pr = torch.from_numpy(P).to(dev), torch.from_numpy(params).to(dev)
+    Href = oracle.hessian_batch(func, P, n, params)
+    hs = np.abs(Href).max(axis=(1, 2))
+    for C in sorted({1, 2, n // 2, n}):
+        if n % C:
+            continue
+        Hs = chf.sym_hessian_batch_seedsparse(func, p, C, pr).cpu().numpy()
+        assert (np.abs(Hs - Href).max(axis=(1, 2)) / hs).max() <= TIGHT, C
+        Hd = chf.sym_hessian_batch(func, p, C, pr).cpu().numpy()
+        assert (np.abs(Hs - Hd).max(axis=(1, 2)) / hs).max() <= TIGHT, C
+        Hg, g = chf.hessian_grad_batch_seedsparse(func, p, C, pr)
+        Hg, g = Hg.cpu().numpy(), g.cpu().numpy()
+        assert (np.abs(Hg - Href).max(axis=(1, 2)) / hs).max() <= TIGHT, C
+        _, g_dev = chf.hessian_grad_batch(func, p, C, pr)
+        g_dev = g_dev.cpu().numpy()
+        gs = np.abs(g_dev).max(axis=1, keepdims=True)
+        assert (np.abs(g - g_dev) / gs).max() <= TIGHT, C
+    g_ref = np.stack([oracle.hessian(func, P[e], params, algo="chunk", C=n)[1] for e in range(3)])
+    assert (np.abs(g[:3] - g_ref) / np.abs(g_ref).max(axis=1, keepdims=True)).max() <= TIGHT
+
+
 @pytest.mark.parametrize("n,m", [(2, 100), (8, 70), (32, 50), (64, 9), (128, 5)])
 def test_seedsparse_f3_hessian(chf, n, m):
     """Seed-sparse Hessian (Alg 5 output): same bits as hessian_batch up to the sign of zero,
