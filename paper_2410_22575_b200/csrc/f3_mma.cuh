@@ -11,11 +11,11 @@
 // FP64 pipe at the same peak (tools/micro/dmma_probe: 37.0 vs 36.7 TFLOP/s, 36.5 mixed; DMMA
 // saturates with one warp per SM sub-partition and 2 independent accumulators,
 // tools/micro/dmma_latency_probe), so this is not a faster pipe -- it is 256 FMAs per issued
-// instruction instead of 32, which frees the issue slots and registers that the SIMT schedule
-// (f3.cuh) spends on broadcasts, loop control and local-memory residual arrays
+// instruction instead of 32, which frees the issue slots and registers that round 1's SIMT
+// schedule (retired) spent on broadcasts, loop control and local-memory residual arrays
 // (profiles/r01/f3: 57% of FP64 peak at n = 64).
 //
-// The evaluation is the f3.cuh slot-column schedule (every scalar op of the hDual evaluation
+// The evaluation is round 1's slot-column schedule (every scalar op of the hDual evaluation
 // once, in the paper's per-slot form; only the order of independent operations changes):
 //   phase A   slots 0 and 1 of every E_k, r_k = E*_k - E_k           (R0, R1 in registers)
 //   phase B   per column c of the chunk: slots 2+c and C+2+c of every E_k, then
@@ -23,7 +23,7 @@
 // The x_slot entries are the slots of the 2n unary ops sin y_j / cos y_j of the seeded inputs
 // (g' u[k] and g' u[C+k] + (g'' u1) u[k], PAPER.md:99 / SPEC.md:81), formed per evaluation by
 // the lane that feeds them to the tensor core; sin a_j, cos a_j (g, g', g'' of the value slot,
-// 0 model FLOPs) are tabulated once per point in shared memory as in f3.cuh.
+// 0 model FLOPs) are tabulated once per point in shared memory.
 //
 // Mapping (m8n8k4: A 8x4 row-major, B 4x8 col-major, C/D 8x8; lane = 4 g + t):
 //   CTA   = W warps x 8 points; M in shared memory in A-fragment order, KB rows at a time.
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(F3Mma<NN, MODE>::W * 32, 1) hvp_f3_mma_kernel(
             const int j = 4 * jq + t;
             const double s0 = sB[j * TS], c0 = cB[j * TS];
             const double y1 = (j == i) ? 1.0 : 0.0, y2 = (j == col) ? 1.0 : 0.0, yC = 0.0;
-            // sin: g' = cos a, g'' = -sin a;   cos: g' = -sin a, g'' = -cos a   (f3.cuh valsB)
+            // sin: g' = cos a, g'' = -sin a;   cos: g' = -sin a, g'' = -cos a   (unary rule)
             const double xa2 = c0 * y2, xaC = c0 * yC + ((-s0) * y1) * y2;
             const double xb2 = (-s0) * y2, xbC = (-s0) * yC + ((-c0) * y1) * y2;
 #pragma unroll

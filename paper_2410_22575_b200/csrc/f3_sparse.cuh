@@ -3,7 +3,7 @@
 // Alg 7 (CHESS-VEC) evaluates f<hDual<C>> on the CHUNK-INIT seeds (Alg 4,
 // PAPER.md:172-194): variable j carries derivative 1 in slot 1 only if j == i (the row) and
 // in slot 2+c only if j == cs+c (the column).  Every other derivative slot of every seed is 0,
-// so in f3.cuh's E_k sums (sum over j of A_kj sin y_j + B_kj cos y_j) all but one term of
+// so in F3's E_k sums (sum over j of A_kj sin y_j + B_kj cos y_j) all but one term of
 // each derivative slot is a product with an exact zero.  This kernel skips those terms:
 //
 //   slot 0 (value)     E0_k = sum_j A_kj s_j + B_kj c_j          same for every row and column
