@@ -9,7 +9,7 @@
 // variable k (Alg 4) on the fly: the paper's per-thread array
 // hDual<C> y[n] is never materialised.
 //
-// Fletcher-Powell is in f3.cuh (its O(n^2) hDual sums need a different schedule).
+// Fletcher-Powell is in csrc/f3_mma.cuh (its O(n^2) hDual sums run on the FP64 tensor core).
 #pragma once
 #include "hdual.cuh"
 
