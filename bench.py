@@ -312,6 +312,11 @@ def main(argv=None):
     flops_pt = chf.model_flops_per_point(args.func, n, C)
     model_tf = m * flops_pt / per_step / 1e12  # per GPU, one launch per step
     clocks = sampler.summary()
+    if world > 1:  # per-rank clocks: median SM MHz and throttle reasons of every GPU
+        allc = [None] * world
+        dist.all_gather_object(allc, {"sm_mhz": clocks["sm_mhz"], "reasons": clocks["reasons"]})
+        clocks["per_rank_sm_mhz"] = [c["sm_mhz"] for c in allc]
+        clocks["reasons"] = sorted({r for c in allc for r in c["reasons"]})
 
     # ---- parity of the timed output against the oracle (rank 0: every point of its shard,
     # F3 at n > 16 on a deterministic sample)
