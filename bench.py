@@ -396,7 +396,7 @@ def main(argv=None):
         small_hbm = run_small_n_hbm(chf, dev, stream, timed_steps, float(peaks.get("hbm_gbs", 0.0)) or None)
 
     # ---- CPU baseline: the oracle on the host cores, rank 0 at N=1 only
-    cpu = None
+    cpu, cpu_per_c = None, []
     if rank == 0 and world == 1 and not args.no_cpu:
         import oracle
         threads = oracle.default_threads()
@@ -404,6 +404,12 @@ def main(argv=None):
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
                "sample": f"first {ms} points of the cfg2 stream: {dt:.1f} s of Alg 7 in the plain C oracle, "
                          f"{threads} pthreads"}
+        if sweep:  # the paper's E5 quantity per C: oracle vs GPU per-point time, sweep file only
+            gpu_rate = {r["csize"]: r["hvp_per_s"] for r in sweep if r["algo"] == "hvp" and r["func"] == args.func}
+            for c in sorted(gpu_rate):
+                rc, mc, dc = oracle_rate(args.func, n, c, params_np[args.func], 0, 1.5, threads)
+                cpu_per_c.append({"csize": c, "oracle_hvp_per_s": rc, "sample_points": mc, "seconds": dc,
+                                  "gpu_hvp_per_s": gpu_rate[c], "gpu_over_oracle": gpu_rate[c] / rc})
 
     # ---- roofline: executed FP64 FLOPs of this build (ncu, profiles/executed_flops.json)
     from paper_2410_22575_b200.build import source_hash
@@ -448,8 +454,8 @@ def main(argv=None):
         if sweep:
             os.makedirs(os.path.dirname(args.sweep_out), exist_ok=True)
             with open(args.sweep_out, "w") as f:
-                json.dump({"headline": line, "sweep": sweep, "paper_l2_baseline": paper_l2, "small_n_hbm": small_hbm},
-                          f, indent=1)
+                json.dump({"headline": line, "sweep": sweep, "paper_l2_baseline": paper_l2, "small_n_hbm": small_hbm,
+                           "oracle_per_csize": cpu_per_c}, f, indent=1)
         print(compact_line(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
