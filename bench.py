@@ -237,7 +237,7 @@ def main(argv=None):
     if rc is not None:
         return rc
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
-    args.device_index = local
+    args.device_index = 0 if os.environ.get("CHESSFAD_BENCH_ONE_GPU") == "1" else local
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -245,10 +245,17 @@ def main(argv=None):
     import torch.distributed as dist
     import paper_2410_22575_b200 as chf
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # test hook (tools/multirank_on_one_gpu.sh): every rank on GPU 0 over gloo, to exercise the
+    # N > 1 logic (shards, gather, max over ranks, the line) on a one-GPU box; never a bench number
+    one_gpu = os.environ.get("CHESSFAD_BENCH_ONE_GPU") == "1"
+    dev_index = 0 if one_gpu else local
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     if rank == 0:
         chf.load()  # builds if stale (file-locked); the other ranks load the result
     if world > 1:
@@ -302,7 +309,7 @@ def main(argv=None):
         return evs[0].elapsed_time(evs[steps]) / 1e3, per
 
     # ---- headline: K steps of chessfad_hvp_batch (Alg 7) on the cfg2 workload
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(args.device_index)
     t_loc, per_loc = timed_steps(lambda: chf.hvp_batch(args.func, pts, vec, C, params[args.func], out=out),
                                  args.steps, args.warmup, sampler)
     t = max_over_ranks(t_loc)
