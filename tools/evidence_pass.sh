@@ -5,6 +5,10 @@
 set -x
 T=${1:-final}; O=gpurun_out/r02$T; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt
+# executed-FLOP entries of kernels changed since the campaign (F3 seed-sparse modes, F3 Alg 8 n > 64)
+bash tools/ncu_executed.sh f3sp16 --n 16 --m 262144 --funcs fletcher_powell --algo hvp_seedsparse > $O/ncu_f3sp16.txt 2>&1
+bash tools/ncu_executed.sh f3sym128 --n 128 --m 4096 --funcs fletcher_powell --algo sym_hvp --csizes 8 16 32 > $O/ncu_f3sym128.txt 2>&1
+cp gpurun_out/executed_flops.json $O/ 2>/dev/null
 python -m pytest tests -m gpu -q > $O/pytest.log 2>&1; echo pytest_rc=$?
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke_rc=$?
 python bench.py --gpus 1 --steps 20 --warmup 5 > $O/bench.log 2>&1; echo bench_rc=$?
