@@ -162,6 +162,23 @@ CHF_INL hd<C> operator/(const hd<C>& u, const hd<C>& v) {
   return r;
 }
 
+// u / c and c / u (a scalar operand is a lifted constant)
+template <int C>
+CHF_INL hd<C> operator/(const hd<C>& u, double c) {
+  hd<C> r;
+#pragma unroll
+  for (int s = 0; s < hd<C>::N; s++) r.v[s] = u.v[s] / c;
+  return r;
+}
+template <int C>
+CHF_INL hd<C> operator/(double c, const hd<C>& v) {
+  hd<C> lifted;
+#pragma unroll
+  for (int s = 0; s < hd<C>::N; s++) lifted.v[s] = 0.0;
+  lifted.v[0] = c;
+  return lifted / v;
+}
+
 // unary chain rule given (g, g', g'') at u0
 template <int C>
 CHF_INL hd<C> hd_unary(const hd<C>& u, double g0, double g1, double g2) {
