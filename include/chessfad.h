@@ -169,7 +169,8 @@ int chessfad_hessian_grad_batch_seedsparse(int func, int n, int csize, int64_t m
  * End-to-end variant of chessfad_hvp_batch on HOST buffers: points, vecs, out (m x n) and
  * params are HOST pointers (pinned memory gives copy/compute overlap; pageable memory
  * works but serialises).  The batch is split into pieces of `piece_points` points
- * (<= 0: library default, m/16) flowing through a three-stage pipeline -- an H2D stream,
+ * (<= 0: library default, m/8; the first and last three pieces ramp down to 1/8 of that so
+ * the pipeline's fill and drain are short) flowing through a three-stage pipeline -- an H2D stream,
  * a compute stream and a D2H stream with three device buffer sets -- so that both copy
  * directions overlap the kernels.  Device scratch: `workspace` (DEVICE, at least
  * chessfad_hvp_host_workspace_bytes(...) bytes, owned by the caller), or NULL to allocate

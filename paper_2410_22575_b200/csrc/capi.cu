@@ -7,6 +7,8 @@
 #include <cstdint>
 #include <cstdlib>
 #include <new>
+#include <utility>
+#include <vector>
 
 #include "../../include/chessfad.h"
 #include "launch.cuh"
@@ -342,8 +344,34 @@ int chessfad_hessian_batch_seedsparse(int func, int n, int csize, int64_t m, con
 namespace {
 constexpr int kHostSets = 3;  // buffer sets of the host pipeline (pieces in flight)
 int64_t host_piece(int64_t m, int64_t piece_points) {
-  if (piece_points <= 0) piece_points = std::max<int64_t>(4096, (m + 15) / 16);
+  if (piece_points <= 0) piece_points = std::max<int64_t>(4096, (m + 7) / 8);
   return std::max<int64_t>(1, std::min(piece_points, m));
+}
+
+// Piece schedule of the host pipeline: pieces of `piece` points, except that the first and the
+// last three ramp (piece/8, /4, /2 ... /2, /4, /8) so that the pipeline's fill (the first H2D,
+// which nothing overlaps) and drain (the last kernel and D2H) move little data.
+std::vector<std::pair<int64_t, int64_t>> host_schedule(int64_t m, int64_t piece) {
+  std::vector<std::pair<int64_t, int64_t>> sched;
+  std::vector<int64_t> head, tail;
+  int64_t body = m;
+  if (m >= 4 * piece && piece >= 64) {
+    for (int64_t d : {8, 4, 2}) {
+      head.push_back(piece / d);
+      tail.insert(tail.begin(), piece / d);
+      body -= 2 * (piece / d);
+    }
+  }
+  int64_t e0 = 0;
+  for (int64_t c : head) sched.push_back({e0, c}), e0 += c;
+  for (int64_t left = body; left > 0;) {
+    const int64_t c = std::min(piece, left);
+    sched.push_back({e0, c});
+    e0 += c;
+    left -= c;
+  }
+  for (int64_t c : tail) sched.push_back({e0, c}), e0 += c;
+  return sched;
 }
 size_t host_ws_bytes(int func, int n, int64_t m, int64_t piece_points) {
   const size_t pbytes = (size_t)host_piece(m, piece_points) * n * sizeof(double);
@@ -408,7 +436,8 @@ int host_pipeline(chessfad_host_ctx* cx, int func, int n, int csize, int64_t m, 
   if (cudaGetDevice(&dev) != cudaSuccess || dev != cx->device) return CHESSFAD_ERR_ARG;
   cudaStream_t s0 = (cudaStream_t)stream;
   const int64_t piece = host_piece(m, piece_points);
-  const int npieces = (int)((m + piece - 1) / piece);
+  const auto sched = host_schedule(m, piece);
+  const int npieces = (int)sched.size();
   const size_t row = (size_t)n * sizeof(double);
   const size_t pdoubles = (size_t)piece * n;
   const size_t nparams = (func == CHESSFAD_FLETCHER_POWELL) ? (size_t)2 * n * n + n : 0;
@@ -429,8 +458,8 @@ int host_pipeline(chessfad_host_ctx* cx, int func, int n, int csize, int64_t m, 
       double* dp = d_buf + (size_t)(3 * b) * pdoubles;
       double* dv = dp + pdoubles;
       double* dout = dv + pdoubles;
-      const int64_t e0 = (int64_t)p * piece;
-      const int64_t cnt = std::min(piece, m - e0);
+      const int64_t e0 = sched[p].first;
+      const int64_t cnt = sched[p].second;
       const size_t bytes = (size_t)cnt * row;
       if (p >= kHostSets) ok(cudaStreamWaitEvent(ss[H2D], cx->ev[D2H][b], 0));  // set b drained
       ok(cudaMemcpyAsync(dp, points + e0 * n, bytes, cudaMemcpyHostToDevice, ss[H2D]));
