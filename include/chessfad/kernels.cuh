@@ -54,9 +54,32 @@ struct BatchArgs {
 constexpr int kPad = 33;     // shared-memory row stride (doubles) of [k][lane] tiles
 constexpr int kWarpsF3 = 4;  // seed-sparse Fletcher-Powell kernel: 128 threads per CTA
 
-// stage points [and vectors] of the tile into shared memory, transposed per 32-point group
+CHF_INL bool aligned16_ptr(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
+
+// stage points [and vectors] of the tile into shared memory, transposed per 32-point group.
+// The tile is one contiguous range of each array (row-major m x n); with n even and 16-byte-
+// aligned rows it is read as coalesced 16-byte words (two coordinates of one point each),
+// otherwise 8 bytes at a time.
 CHF_INL void stage_tile(const BatchArgs& p, int64_t e0, int P, double* s_pts, double* s_vec) {
   const int n = p.n;
+  if ((n & 1) == 0 && aligned16_ptr(p.points) && (!s_vec || aligned16_ptr(p.vecs))) {
+    const int h = n >> 1;
+    for (int q = threadIdx.x; q < P * h; q += blockDim.x) {
+      const int pi = q / h, k = 2 * (q - pi * h);
+      int64_t e = e0 + pi;
+      if (e >= p.m) e = p.m - 1;  // ragged tail: replicate the last point, never stored
+      const int g = pi >> 5, ln = pi & 31;
+      const double2 x = __ldg(reinterpret_cast<const double2*>(p.points + e * n + k));
+      s_pts[(g * n + k) * kPad + ln] = x.x;
+      s_pts[(g * n + k + 1) * kPad + ln] = x.y;
+      if (s_vec) {
+        const double2 w = __ldg(reinterpret_cast<const double2*>(p.vecs + e * n + k));
+        s_vec[(g * n + k) * kPad + ln] = w.x;
+        s_vec[(g * n + k + 1) * kPad + ln] = w.y;
+      }
+    }
+    return;
+  }
   for (int q = threadIdx.x; q < P * n; q += blockDim.x) {
     const int pi = q / n, k = q - pi * n;
     int64_t e = e0 + pi;
@@ -69,6 +92,16 @@ CHF_INL void stage_tile(const BatchArgs& p, int64_t e0, int P, double* s_pts, do
 
 CHF_INL void write_tile(const BatchArgs& p, int64_t e0, int P, const double* s_out) {
   const int n = p.n;
+  if ((n & 1) == 0 && aligned16_ptr(p.out)) {  // 16-byte coalesced stores
+    const int h = n >> 1;
+    for (int q = threadIdx.x; q < P * h; q += blockDim.x) {
+      const int pi = q / h, k = 2 * (q - pi * h);
+      const int64_t e = e0 + pi;
+      const double* src = s_out + ((pi >> 5) * n + k) * kPad + (pi & 31);
+      if (e < p.m) *reinterpret_cast<double2*>(p.out + e * n + k) = make_double2(src[0], src[kPad]);
+    }
+    return;
+  }
   for (int q = threadIdx.x; q < P * n; q += blockDim.x) {
     const int pi = q / n, k = q - pi * n;
     const int64_t e = e0 + pi;
