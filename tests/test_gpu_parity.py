@@ -175,6 +175,42 @@ def test_edge_cases(chf):
                       torch.zeros((4, 4), dtype=torch.float32, device=dev), 2)
 
 
+@pytest.mark.parametrize("family,func,n,C", [("stream", "rosenbrock", 2, 1), ("stream", "ackley", 4, 2),
+                                              ("stream", "prodsum", 8, 8), ("reg", "rosenbrock", 5, 5),
+                                              ("reg", "ackley", 16, 16), ("f3_dmma", "fletcher_powell", 16, 4),
+                                              ("f3_dmma", "fletcher_powell", 72, 8)])
+def test_small_m_every_family(chf, family, func, n, C):
+    """Tiny and ragged batches on every kernel family: m = 1, 2, 7, 63, 65, 257 (one partial
+    tile / CTA / warp, exact multiples +- 1), HVP and Hessian, against the oracle."""
+    assert chf.path(func, n, C) == family
+    params = _params(func, n)
+    dev = torch.device("cuda")
+    pr = None if params is None else torch.from_numpy(params).to(dev)
+    for m in (1, 2, 7, 63, 65, 257):
+        if func == "fletcher_powell" and n > 16 and m > 65:
+            continue
+        P, V = synth.points(50 + m, n, m), synth.vectors(50 + m, n, m)
+        ref, sabs = oracle.hvp_batch(func, P, V, C, params)
+        _check(_gpu_hvp(chf, func, P, V, C, params), ref, sabs)
+        k = min(m, 7)
+        H = chf.hessian_batch(func, torch.from_numpy(P[:k]).to(dev), C, pr).cpu().numpy()
+        Href = oracle.hessian_batch(func, P[:k], C, params)
+        scale = np.maximum(np.abs(Href).max(axis=(1, 2)), 1e-300)
+        assert (np.abs(H - Href).max(axis=(1, 2)) / scale).max() <= TIGHT, m
+
+
+def test_nan_propagates_every_family(chf):
+    """Ackley at the origin has NaN derivatives: they propagate (no error) through
+    the stream kernel (n = 2), the register kernel (n = 16) and a NaN input through F3."""
+    for n, C in ((2, 1), (16, 4)):
+        got = _gpu_hvp(chf, "ackley", np.zeros((3, n)), np.ones((3, n)), C)
+        assert np.all(np.isnan(got)), n
+    P = synth.points(3, 16, 64)
+    P[5, 3] = np.nan
+    got = _gpu_hvp(chf, "fletcher_powell", P, np.ones((64, 16)), 4, _params("fletcher_powell", 16))
+    assert np.all(np.isnan(got[5])) and np.all(np.isfinite(np.delete(got, 5, axis=0)))
+
+
 def test_determinism_and_shards(chf):
     """No atomics, fixed order: bitwise identical run to run, and a batch computed in
     shards (as the multi-GPU driver does) equals the unsharded batch bit for bit."""
