@@ -421,6 +421,8 @@ def main(argv=None):
     # ---- roofline: executed FP64 FLOPs of this build (ncu, profiles/executed_flops.json)
     from paper_2410_22575_b200.build import source_hash
     ex = executed_entry(args.func, n, C, source_hash())
+    if ex is not None and ex["basis"].startswith("STALE"):
+        ex = None  # measured on other kernel SASS: no executed-FLOP claim for this build
     exec_tf = None if ex is None else m * ex["executed_flops_per_point"] / per_step / 1e12
     traffic = None if ex is None else ex["dram_bytes_per_launch"] * m / ex["m"]
     achieved = exec_tf if exec_tf is not None else model_tf
@@ -446,7 +448,8 @@ def main(argv=None):
                          "hbm_gbs": alg_bytes / per_step / 1e9,
                          "fp64_pipe_pct_ncu": None if ex is None else ex["fp64_pipe_active_pct"],
                          "basis": "frac: ncu-executed 2*DFMA+DMUL+DADD (" + (
-                             ("SASS " + ex["sass_hash"]) if ex and ex.get("sass_hash") else "n/a") +
+                             ("SASS " + ex["sass_hash"]) if ex and ex.get("sass_hash") else
+                             "no ncu entry for this kernel SASS: frac = frac_model") +
                              "); frac_model: §8(d) model (DESIGN.md §5)",
                          "peak_basis": f"{SMS}x{FP64_FMA_PER_SM_CLK}x2x{peak_mhz:.0f}MHz",
                          "fp64_probe_tflops": probe_tf},

@@ -17,11 +17,11 @@ struct UserF {
       s = cos(y0) + y0 / (1.0 + y0 * y0);
     }
     for (int i = 1; i < n; i++) {
-      const hd<C> yi = y(i);
+      const auto yi = y(i);
       s = s + (cos(yi) + yi / (1.0 + yi * yi));
     }
     for (int i = 0; i < n - 1; i++) {
-      const hd<C> a = y(i);
+      const auto a = y(i);
       s = s + a * a * y(i + 1);
     }
     return s;

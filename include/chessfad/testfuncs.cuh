@@ -30,16 +30,14 @@ struct LaneSeed {
   // (g, g', g'' of an input-only argument; the model counts them as 0 FLOPs)
   const double* sin2pi;
   const double* cos2pi;
-  CHF_INL hd<C> operator()(int k) const {
-    hd<C> y;
+  CHF_INL hs<C> operator()(int k) const {
+    hs<C> y;
     y.v[0] = a[k * stride];
     y.v[1] = (k == i) ? 1.0 : 0.0;
     const int off = k - cs;
 #pragma unroll
     for (int l = 0; l < C; l++) y.v[2 + l] = (off == l) ? 1.0 : 0.0;
-#pragma unroll
-    for (int l = 0; l < C; l++) y.v[C + 2 + l] = 0.0;
-    return y;
+    return y;  // second-order slots: structural zeros (hdual.cuh hs<C>)
   }
 };
 
@@ -59,14 +57,12 @@ struct StaticSeed {
   int i, cs;
   const double* sin2pi;
   const double* cos2pi;
-  CHF_INL hd<C> operator()(int k) const {
-    hd<C> y;
+  CHF_INL hs<C> operator()(int k) const {
+    hs<C> y;
     y.v[0] = a[k];
     y.v[1] = (k == i) ? 1.0 : 0.0;
 #pragma unroll
     for (int l = 0; l < C; l++) y.v[2 + l] = (k - cs == l) ? 1.0 : 0.0;
-#pragma unroll
-    for (int l = 0; l < C; l++) y.v[C + 2 + l] = 0.0;
     return y;
   }
 };
@@ -101,28 +97,28 @@ CHF_INL hd<C> f_rosenbrock(int n, const Seed& y) {
   hd<C> s;
   if constexpr (Seed::kFused) {
     {
-      const hd<C> y0 = y(0), y1 = y(1);
-      const hd<C> d = hd_fnma(y0, y0, y1);
-      const hd<C> e = 1.0 - y0;
+      const auto y0 = y(0), y1 = y(1);
+      const auto d = hd_fnma(y0, y0, y1);
+      const auto e = 1.0 - y0;
       s = hd_fma(e, e, 100.0 * (d * d));
     }
     seed_loop<Seed, CHF_SUM_UNROLL>(1, n - 1, [&](int i) {
-      const hd<C> yi = y(i), yi1 = y(i + 1);
-      const hd<C> d = hd_fnma(yi, yi, yi1);
-      const hd<C> e = 1.0 - yi;
+      const auto yi = y(i), yi1 = y(i + 1);
+      const auto d = hd_fnma(yi, yi, yi1);
+      const auto e = 1.0 - yi;
       s = hd_fma(e, e, hd_axpy(100.0, d * d, s));
     });
   } else {  // the canonical form as written (R2)
     {
-      const hd<C> y0 = y(0), y1 = y(1);
+      const auto y0 = y(0), y1 = y(1);
       const hd<C> d = y1 - y0 * y0;
-      const hd<C> e = 1.0 - y0;
+      const auto e = 1.0 - y0;
       s = 100.0 * (d * d) + e * e;
     }
     seed_loop<Seed, 2>(1, n - 1, [&](int i) {
-      const hd<C> yi = y(i), yi1 = y(i + 1);
+      const auto yi = y(i), yi1 = y(i + 1);
       const hd<C> d = yi1 - yi * yi;
-      const hd<C> e = 1.0 - yi;
+      const auto e = 1.0 - yi;
       const hd<C> t = 100.0 * (d * d) + e * e;
       s = s + t;
     });
@@ -137,25 +133,25 @@ CHF_INL hd<C> f_ackley(int n, const Seed& y) {
   const double two_pi = 6.283185307179586, euler = 2.718281828459045;
   hd<C> s1;
   {
-    const hd<C> y0 = y(0);
+    const auto y0 = y(0);
     s1 = y0 * y0;
   }
   seed_loop<Seed, 0>(1, n, [&](int i) {
-    const hd<C> yi = y(i);
+    const auto yi = y(i);
     if constexpr (Seed::kFused) s1 = hd_fma(yi, yi, s1);  // s1 + yi*yi, fused (R5)
     else s1 = s1 + yi * yi;
   });
   // cos(u), u = 2 pi y_i: (g, g', g'') = (cos u0, -sin u0, -cos u0) with u0 = 2 pi a_i,
   // bit-identical to the tabulated argument (same single rounding of two_pi * a_i)
   auto cos2pi = [&](int k) {
-    const hd<C> u = two_pi * y(k);
+    const auto u = two_pi * y(k);
     const double s = y.sin2pi[k * y.stride], c = y.cos2pi[k * y.stride];
     return hd_unary(u, c, -s, -c);
   };
   hd<C> s2 = cos2pi(0);
   seed_loop<Seed, 0>(1, n, [&](int i) {
     if constexpr (Seed::kFused) {  // s2 + cos(2 pi y_i), fused (R5)
-      const hd<C> u = two_pi * y(i);
+      const auto u = two_pi * y(i);
       s2 = hd_unary_acc(u, y.cos2pi[i * y.stride], -y.sin2pi[i * y.stride], -y.cos2pi[i * y.stride], s2);
     } else {
       s2 = s2 + cos2pi(i);
@@ -240,9 +236,9 @@ template <int C>
 CHF_INL hd<C> fsp_rosenbrock(int n, const LaneSeed<C>& y) {
   hd<C> s = hd_zero<C>();
   sp_union(y.i - 1, y.i, y.cs - 1, y.cs + C - 1, n - 2, [&](int k) {
-    const hd<C> yk = y(k), yk1 = y(k + 1);
-    const hd<C> d = hd_fnma(yk, yk, yk1);
-    const hd<C> e = 1.0 - yk;
+    const auto yk = y(k), yk1 = y(k + 1);
+    const auto d = hd_fnma(yk, yk, yk1);
+    const auto e = 1.0 - yk;
     s = hd_fma(e, e, hd_axpy(100.0, d * d, s));
   });
   return s;
@@ -262,9 +258,9 @@ CHF_INL hd<C> fsp_ackley(int n, const LaneSeed<C>& y) {
   const double two_pi = 6.283185307179586, euler = 2.718281828459045;
   hd<C> s1 = hd_zero<C>(), s2 = hd_zero<C>();
   sp_union(y.i, y.i, y.cs, y.cs + C - 1, n - 1, [&](int k) {
-    const hd<C> yk = y(k);
+    const auto yk = y(k);
     s1 = hd_fma(yk, yk, s1);
-    const hd<C> u = two_pi * yk;
+    const auto u = two_pi * yk;
     s2 = hd_unary_acc(u, y.cos2pi[k * y.stride], -y.sin2pi[k * y.stride], -y.cos2pi[k * y.stride], s2);
   });
   {  // value slots: the chains of f_ackley (first term initialises)

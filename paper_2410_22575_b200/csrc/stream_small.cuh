@@ -55,15 +55,13 @@ struct RegSeed {
   int i, cs;                             // row / chunk start (runtime values)
   const double* sin2pi;                  // Ackley: sincos(2 pi a_k) of the point (registers)
   const double* cos2pi;
-  CHF_INL hd<C> operator()(int k) const {
-    hd<C> y;
+  CHF_INL hs<C> operator()(int k) const {
+    hs<C> y;  // second-order slots: structural zeros (hdual.cuh hs<C>)
     y.v[0] = a[k];
     y.v[1] = (k == i) ? 1.0 : 0.0;
     const int off = k - cs;
 #pragma unroll
     for (int l = 0; l < C; l++) y.v[2 + l] = (off == l) ? 1.0 : 0.0;
-#pragma unroll
-    for (int l = 0; l < C; l++) y.v[C + 2 + l] = 0.0;
     return y;
   }
 };
