@@ -96,15 +96,18 @@ template <int C, class Seed>
 CHF_INL hd<C> f_rosenbrock(int n, const Seed& y) {
   hd<C> s;
   if constexpr (Seed::kFused) {
+    auto yc = y(1);  // the seed of y_{i+1}, carried into the next term (one seed built per term;
+                     // 3-5% faster for Rosenbrock, slower for prodsum: profiles/r02/seed_typed/carry)
     {
-      const auto y0 = y(0), y1 = y(1);
-      const auto d = hd_fnma(y0, y0, y1);
+      const auto y0 = y(0);
+      const auto d = hd_fnma(y0, y0, yc);
       const auto e = 1.0 - y0;
       s = hd_fma(e, e, 100.0 * (d * d));
     }
     seed_loop<Seed, CHF_SUM_UNROLL>(1, n - 1, [&](int i) {
-      const auto yi = y(i), yi1 = y(i + 1);
-      const auto d = hd_fnma(yi, yi, yi1);
+      const auto yi = yc;
+      yc = y(i + 1);
+      const auto d = hd_fnma(yi, yi, yc);
       const auto e = 1.0 - yi;
       s = hd_fma(e, e, hd_axpy(100.0, d * d, s));
     });

@@ -124,6 +124,121 @@ struct RosenZ {
   }
 };
 
+// ---- prototype: chunk slots of the seed read from a shared one-hot table with 16-byte loads
+// T[q][t] = [t == Z + q]  (q = 0, 1: two copies so that the C-slot window starts 16-byte aligned)
+constexpr int kTabZ = 20, kTabN = 48;
+template <int C>
+struct TabSeed {
+  static constexpr bool kStatic = false;
+  static constexpr bool kFused = true;
+  const double* a;
+  int stride;
+  int i, cs;
+  const double* sin2pi;
+  const double* cos2pi;
+  const double* tab;  // shared [2][kTabN]
+  CHF_INL hs<C> operator()(int k) const {
+    hs<C> y;
+    y.v[0] = a[k * stride];
+    y.v[1] = (k == i) ? 1.0 : 0.0;
+    int off = k - cs;
+    off = min(max(off, -1), C);               // outside the chunk: every slot 0
+    const int q = off & 1;                    // copy whose window start Z + q - off is even
+    const double2* w = reinterpret_cast<const double2*>(tab + q * kTabN + kTabZ + q - off);
+#pragma unroll
+    for (int l = 0; l < C / 2; l++) {
+      const double2 t = w[l];
+      y.v[2 + 2 * l] = t.x;
+      y.v[3 + 2 * l] = t.y;
+    }
+    return y;
+  }
+};
+
+template <class F, int C, int W>
+__global__ void __launch_bounds__(W * 32, 1) tab_kernel(BatchArgs p, F f) {
+  extern __shared__ double smem[];
+  __shared__ __align__(16) double s_tab[2 * kTabN];
+  const int n = p.n, P = 32;
+  double* s_pts = smem;
+  double* s_vec = s_pts + n * kPad;
+  double* s_out = s_vec + n * kPad;
+  const int64_t e0 = (int64_t)blockIdx.x * P;
+  for (int t = threadIdx.x; t < 2 * kTabN; t += blockDim.x) s_tab[t] = (t % kTabN == kTabZ + t / kTabN) ? 1.0 : 0.0;
+  stage_tile(p, e0, P, s_pts, s_vec);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* a = s_pts + lane;
+  const double* v = s_vec + lane;
+  double* o = s_out + lane;
+  const int64_t e = e0 + lane;
+  for (int i = warp; i < n; i += W) {
+    RowSink<MODE_HVP> sink = make_sink<MODE_HVP>(p, i, e, v, o);
+    for (int j = 0; j < n / C; j++) {
+      const int cs = j * C;
+      const TabSeed<C> y{a, kPad, i, cs, nullptr, nullptr, s_tab};
+      const hd<C> t = f.template operator()<C>(n, y);
+#pragma unroll
+      for (int l = 0; l < C; l++) sink(cs + l, t.v[C + 2 + l]);
+    }
+    o[i * kPad] = sink.res;
+  }
+  __syncthreads();
+  write_tile(p, e0, P, s_out);
+}
+
+// Rosenbrock with the seed of y_{i+1} carried into the next term (one seed built per term)
+struct RosenCarry {
+  static constexpr bool kTrig2Pi = false;
+  template <int C, class Seed>
+  CHF_INL hd<C> operator()(int n, const Seed& y) const {
+    hd<C> s;
+    auto yc = y(1);
+    {
+      const auto y0 = y(0);
+      const auto d = hd_fnma(y0, y0, yc);
+      const auto e = 1.0 - y0;
+      s = hd_fma(e, e, 100.0 * (d * d));
+    }
+#pragma unroll 4
+    for (int i = 1; i < n - 1; i++) {
+      const auto yi = yc;
+      yc = y(i + 1);
+      const auto d = hd_fnma(yi, yi, yc);
+      const auto e = 1.0 - yi;
+      s = hd_fma(e, e, hd_axpy(100.0, d * d, s));
+    }
+    return s;
+  }
+};
+
+// Ackley with S1 and S2 accumulated in one pass over the variables (one seed per variable;
+// each sum keeps its own ascending order -> bit-identical)
+struct AckleyOnePass {
+  static constexpr bool kTrig2Pi = true;
+  template <int C, class Seed>
+  CHF_INL hd<C> operator()(int n, const Seed& y) const {
+    const double two_pi = 6.283185307179586, euler = 2.718281828459045;
+    hd<C> s1, s2;
+    {
+      const auto y0 = y(0);
+      s1 = y0 * y0;
+      const auto u = two_pi * y0;
+      s2 = hd_unary(u, y.cos2pi[0], -y.sin2pi[0], -y.cos2pi[0]);
+    }
+    for (int i = 1; i < n; i++) {
+      const auto yi = y(i);
+      s1 = hd_fma(yi, yi, s1);
+      const auto u = two_pi * yi;
+      s2 = hd_unary_acc(u, y.cos2pi[i * y.stride], -y.sin2pi[i * y.stride], -y.cos2pi[i * y.stride], s2);
+    }
+    const double inv_n = 1.0 / n;
+    const hd<C> t1 = (-20.0) * exp((-0.2) * sqrt(s1 * inv_n));
+    const hd<C> t2 = exp(s2 * inv_n);
+    return (t1 - t2) + (20.0 + euler);
+  }
+};
+
 // persistent CTAs, static tile order, the next tile's points/vectors prefetched with 8-byte
 // cp.async into the other half of a double buffer while the current tile is evaluated
 CHF_INL void cp_async8(double* dst, const double* src) {
@@ -234,6 +349,48 @@ int main(int argc, char** argv) {
     timeit("persist", 1, [&] { k<<<pgrid, 128, psmem>>>(a, F{}); });
   }
   timeit("zseed", 1, [&] { CK((launch_functor<RosenZ, 16, MODE_HVP>(RosenZ{}, a, 0))); });
+  timeit("carry", 1, [&] { CK((launch_functor<RosenCarry, 16, MODE_HVP>(RosenCarry{}, a, 0))); });
+  {
+    std::vector<double> ref(m * n), got(m * n);
+    CK((launch_functor<F, 16, MODE_HVP>(F{}, a, 0)));
+    CK(cudaMemcpy(ref.data(), dout, m * n * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemset(dout, 0, m * n * 8));
+    CK((launch_functor<RosenCarry, 16, MODE_HVP>(RosenCarry{}, a, 0)));
+    CK(cudaMemcpy(got.data(), dout, m * n * 8, cudaMemcpyDeviceToHost));
+    int64_t bad = 0;
+    for (int64_t q = 0; q < m * n; q++) bad += ref[q] != got[q];
+    printf("carry parity: %lld bitwise mismatches of %lld\n", (long long)bad, (long long)(m * n));
+  }
+  auto cmp = [&](const char* name, auto&& la, auto&& lb) {
+    std::vector<double> ref(m * n), got(m * n);
+    la();
+    CK(cudaMemcpy(ref.data(), dout, m * n * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemset(dout, 0, m * n * 8));
+    lb();
+    CK(cudaMemcpy(got.data(), dout, m * n * 8, cudaMemcpyDeviceToHost));
+    int64_t bad = 0;
+    for (int64_t q = 0; q < m * n; q++) bad += !(ref[q] == got[q] || (ref[q] != ref[q] && got[q] != got[q]));
+    printf("%s parity: %lld bitwise mismatches of %lld\n", name, (long long)bad, (long long)(m * n));
+  };
+  using FA = BuiltinFunc<FUNC_ACKLEY>;
+  timeit("ackley8", 1, [&] { CK((launch_functor<FA, 8, MODE_HVP>(FA{}, a, 0))); });
+  timeit("ack1pass8", 1, [&] { CK((launch_functor<AckleyOnePass, 8, MODE_HVP>(AckleyOnePass{}, a, 0))); });
+  timeit("ackley16", 1, [&] { CK((launch_functor<FA, 16, MODE_HVP>(FA{}, a, 0))); });
+  timeit("ack1pass16", 1, [&] { CK((launch_functor<AckleyOnePass, 16, MODE_HVP>(AckleyOnePass{}, a, 0))); });
+  cmp("ack1pass8", [&] { CK((launch_functor<FA, 8, MODE_HVP>(FA{}, a, 0))); },
+      [&] { CK((launch_functor<AckleyOnePass, 8, MODE_HVP>(AckleyOnePass{}, a, 0))); });
+  timeit("tab", 1, [&] { tab_kernel<F, 16, 4><<<grid, 128, smem>>>(a, F{}); });
+  {
+    std::vector<double> ref(m * n), got(m * n);
+    CK((launch_functor<F, 16, MODE_HVP>(F{}, a, 0)));
+    CK(cudaMemcpy(ref.data(), dout, m * n * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemset(dout, 0, m * n * 8));
+    tab_kernel<F, 16, 4><<<grid, 128, smem>>>(a, F{});
+    CK(cudaMemcpy(got.data(), dout, m * n * 8, cudaMemcpyDeviceToHost));
+    int64_t bad = 0;
+    for (int64_t q = 0; q < m * n; q++) bad += ref[q] != got[q];
+    printf("tab parity: %lld bitwise mismatches of %lld\n", (long long)bad, (long long)(m * n));
+  }
   {
     std::vector<double> ref(m * n), got(m * n);
     CK((launch_functor<F, 16, MODE_HVP>(F{}, a, 0)));
