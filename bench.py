@@ -425,7 +425,7 @@ def main(argv=None):
         ex = None  # measured on other kernel SASS: no executed-FLOP claim for this build
     exec_tf = None if ex is None else m * ex["executed_flops_per_point"] / per_step / 1e12
     traffic = None if ex is None else ex["dram_bytes_per_launch"] * m / ex["m"]
-    achieved = exec_tf if exec_tf is not None else model_tf
+    achieved = exec_tf  # None without an ncu entry for this kernel SASS (no FLOP-rate claim then)
     alg_bytes = 24 * n * m  # a1 + a7: read points and vectors, write out (§8(d))
 
     if rank == 0:
@@ -440,7 +440,7 @@ def main(argv=None):
             "higher_is_better": True, "scaling": "strong" if args.m_total else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_config(args, world),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf,
+                         "frac": None if achieved is None else achieved / peak_tf,
                          "frac_executed": None if exec_tf is None else exec_tf / peak_tf,
                          "frac_model": model_tf / peak_tf,
                          "executed_over_model": None if ex is None else ex["executed_flops_per_point"] / flops_pt,
@@ -449,7 +449,7 @@ def main(argv=None):
                          "fp64_pipe_pct_ncu": None if ex is None else ex["fp64_pipe_active_pct"],
                          "basis": "frac: ncu-executed 2*DFMA+DMUL+DADD (" + (
                              ("SASS " + ex["sass_hash"]) if ex and ex.get("sass_hash") else
-                             "no ncu entry for this kernel SASS: frac = frac_model") +
+                             "no ncu entry for this kernel SASS: frac null") +
                              "); frac_model: §8(d) model (DESIGN.md §5)",
                          "peak_basis": f"{SMS}x{FP64_FMA_PER_SM_CLK}x2x{peak_mhz:.0f}MHz",
                          "fp64_probe_tflops": probe_tf},
@@ -617,7 +617,10 @@ def kernel_matches_path(kernel: str, path: str) -> bool:
         if prefix + "<" in kernel:
             return fam == path
     if "hvp_reg_kernel<" in kernel:
-        return path == ("reg_seedsparse" if "SparseFunc" in kernel else "reg")
+        if "SparseFunc" in kernel:
+            return path == "reg_seedsparse"
+        ns = kernel.split("hvp_reg_kernel<", 1)[1].split(">(", 1)[0].rsplit(",", 1)[-1].strip()
+        return path == ("reg_ns" if ns not in ("0", "4") else "reg")  # last argument: NS (W on older builds)
     return False
 
 

@@ -154,12 +154,17 @@ CHF_INL RowSink<MODE> make_sink(const BatchArgs& p, int i, int64_t e, const doub
 #ifndef CHF_REG_MINB
 #define CHF_REG_MINB 1  // min CTAs/SM hint of the register path (tuning experiments)
 #endif
-template <class F, int C, int MODE, int W>
+// NS > 0: n == NS at compile time (the paper's NV-templated kernels, Fig. 2):
+// the function's variable loops are fully unrolled and each seed's variable index is a
+// constant; rows and chunks remain runtime loops, so every (row, chunk) evaluation of Alg 7 is
+// still formed from its own CHUNK-INIT seeds and executed on its own.  nvcc folds the seed
+// slots that become constants (x*1 -> x; IEEE-exact, outputs bit-identical to NS = 0).
+template <class F, int C, int MODE, int W, int NS = 0>
 __global__ void __launch_bounds__(W * 32, CHF_REG_MINB) hvp_reg_kernel(BatchArgs p, F f) {
   constexpr bool TRIG = uses_trig2pi<F>::value;
   constexpr bool HESS = mode_hess(MODE);
   extern __shared__ double smem[];
-  const int n = p.n, G = p.groups, P = 32 * G, Capi = p.csize;
+  const int n = NS > 0 ? NS : p.n, G = p.groups, P = 32 * G, Capi = p.csize;
   double* s_pts = smem;
   double* s_vec = HESS ? nullptr : s_pts + G * n * kPad;
   double* s_out = HESS ? nullptr : s_vec + G * n * kPad;
@@ -191,10 +196,11 @@ __global__ void __launch_bounds__(W * 32, CHF_REG_MINB) hvp_reg_kernel(BatchArgs
     const int scn = i / Capi;  // row i's first chunk (symmetric modes)
     RowSink<MODE> sink = make_sink<MODE>(p, i, e, v, o);
     double gi = 0.0;  // MODE_HESS_GRAD: df/dx_i (slot v[1], identical for every chunk of row i)
+#pragma unroll 1
     for (int j = mode_sym(MODE) ? (scn * Capi) / C : 0; j < nchunk; j++) {
       const int cs = j * C;
       sink.mirror = cs / Capi > scn;
-      const LaneSeed<C> y{a, kPad, i, cs, tsin, tcos};
+      const LaneSeed<C, (NS > 0)> y{a, kPad, i, cs, tsin, tcos};
       const hd<C> t = f.template operator()<C>(n, y);  // CHUNK-INIT + f<hDual<C>>, Alg 7 :389-390
 #pragma unroll
       for (int l = 0; l < C; l++) sink(cs + l, t.v[C + 2 + l]);  // :392-394 / :210-212 / :417-421

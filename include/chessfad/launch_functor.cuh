@@ -42,12 +42,13 @@ inline cudaError_t launch_with_smem(K kernel, int grid, int block, size_t smem, 
 }
 
 // any functor F (built-in or user, see testfuncs.cuh), hDual<C> in registers
-template <class F, int C, int MODE>
+// NS > 0: the kernel compiled for n == NS (kernels.cuh); the caller guarantees a.n == NS
+template <class F, int C, int MODE, int NS = 0>
 cudaError_t launch_functor(const F& f, BatchArgs a, cudaStream_t s) {
   a.groups = groups_for(a.n, kWarpsReg, MODE);
   const int64_t P = 32 * a.groups;
   const int grid = (int)((a.m + P - 1) / P);
-  return launch_with_smem(hvp_reg_kernel<F, C, MODE, kWarpsReg>, grid, kWarpsReg * 32,
+  return launch_with_smem(hvp_reg_kernel<F, C, MODE, kWarpsReg, NS>, grid, kWarpsReg * 32,
                           reg_smem_bytes(uses_trig2pi<F>::value, a.n, a.groups, MODE), s, a, f);
 }
 

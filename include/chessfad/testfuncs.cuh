@@ -19,9 +19,13 @@ enum { FUNC_ROSENBROCK = 0, FUNC_ACKLEY = 1, FUNC_FLETCHER_POWELL = 2, FUNC_PROD
 
 // CHUNK-INIT seed for the lane's own point; row i and chunk start cs are warp-uniform.
 //   y[k] = < a_k, [k==i], e_{k-cs} if cs <= k < cs+C, 0 ... 0 >          (Alg 4)
-template <int C>
+// STATIC: n is a compile-time constant of the kernel (the paper's NV template, Fig. 2,
+// PAPER.md:485-499) and the functions' variable loops are fully unrolled, so k is a constant
+// in each copy; row i and chunk start cs stay runtime values (every evaluation is formed and
+// executed on its own, as in Alg 7).
+template <int C, bool STATIC = false>
 struct LaneSeed {
-  static constexpr bool kStatic = false;  // runtime n: loops keep their partial unrolling
+  static constexpr bool kStatic = STATIC;  // false: runtime n, loops keep their partial unrolling
   static constexpr bool kFused = true;    // fused accumulate forms (R5) in the running sums
   const double* a;  // a[k * stride] = coordinate k of this lane's point (shared memory)
   int stride;

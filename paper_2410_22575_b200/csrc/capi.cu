@@ -178,6 +178,16 @@ bool stream_small_n(int func, int n, int C) {
   return n == 2 || n == 4 || (n == 8 && func == CHESSFAD_PRODSUM);
 }
 
+#ifndef CHF_REGN
+#define CHF_REGN 1  // register path: kernels compiled for n in {8, 16, 32} (0: runtime-n kernel only)
+#endif
+// Used where it measured faster (profiles/r02/ns/summary.txt: 1.1-5.8x for every HVP mode and
+// F1/F2 Hessians); prodsum's Hessian modes measured up to 1.3x slower and keep the runtime-n kernel.
+bool regn_use(int func, int n, int mode) {
+  if (!CHF_REGN || !(n == 8 || n == 16 || n == 32)) return false;
+  return !(func == CHESSFAD_PRODSUM && mode_hess(mode));
+}
+
 bool aligned16(const BatchArgs& a) {
   return ((reinterpret_cast<uintptr_t>(a.points) | reinterpret_cast<uintptr_t>(a.vecs) |
            reinterpret_cast<uintptr_t>(a.out)) & 15) == 0;
@@ -206,6 +216,23 @@ cudaError_t dispatch_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s)
     }
     return dispatch_reg<MODE_HVP>(func, Capi, a, s);  // no hoisted kernel: per-evaluation path
   } else {
+    if (regn_use(func, a.n, MODE)) {  // the kernel compiled for this n (kernels.cuh NS)
+#define CHF_CASE_NS(F, NS)                                     \
+  if (a.n == NS) switch (C) {                                  \
+      case 1: return launch_reg_n<F, 1, MODE, NS>(a, s);       \
+      case 2: return launch_reg_n<F, 2, MODE, NS>(a, s);       \
+      case 4: return launch_reg_n<F, 4, MODE, NS>(a, s);       \
+      case 8: return launch_reg_n<F, 8, MODE, NS>(a, s);       \
+      case 16: return launch_reg_n<F, 16, MODE, NS>(a, s);     \
+    }
+      switch (func) {
+        case CHESSFAD_ROSENBROCK: CHF_FOR_REGN_NS(CHF_CASE_NS, FUNC_ROSENBROCK) break;
+        case CHESSFAD_ACKLEY: CHF_FOR_REGN_NS(CHF_CASE_NS, FUNC_ACKLEY) break;
+        case CHESSFAD_PRODSUM: CHF_FOR_REGN_NS(CHF_CASE_NS, FUNC_PRODSUM) break;
+      }
+#undef CHF_CASE_NS
+      return cudaErrorInvalidValue;
+    }
 #define CHF_CASE_C(F)                                  \
   switch (C) {                                         \
     case 1: return launch_reg<F, 1, MODE>(a, s);       \
@@ -606,7 +633,9 @@ const char* chessfad_path(int func, int n, int csize, int algo) {
   const int C = reg_kernel_chunk(csize);
   if (algo == CHESSFAD_ALGO_HVP && stream_small_n(func, n, C)) return "stream";  // 16-byte-aligned buffers
   if (algo == CHESSFAD_ALGO_HVP_HOISTED && (n == 2 || n == 4 || n == 8 || n == 16)) return "small_hoisted";
-  return "reg";
+  const int mode = algo == CHESSFAD_ALGO_HESSIAN ? MODE_HESS : algo == CHESSFAD_ALGO_SYM_HESSIAN ? MODE_SYM_HESS
+                   : algo == CHESSFAD_ALGO_HESSIAN_GRAD ? MODE_HESS_GRAD : MODE_HVP;
+  return regn_use(func, n, mode) ? "reg_ns" : "reg";
 }
 
 const char* chessfad_version(void) { return "chessfad-b200 0.1.0 (sm_100a)"; }

@@ -16,6 +16,21 @@ template <int FUNC, int C, int MODE>
 cudaError_t launch_reg(BatchArgs a, cudaStream_t s) {
   return launch_functor<BuiltinFunc<FUNC>, C, MODE>(BuiltinFunc<FUNC>{}, a, s);
 }
+// the same kernel compiled for n == NS (kernels.cuh NS; inst_regn_*.cu)
+template <int FUNC, int C, int MODE, int NS>
+cudaError_t launch_reg_n(BatchArgs a, cudaStream_t s) {
+  return launch_functor<BuiltinFunc<FUNC>, C, MODE, NS>(BuiltinFunc<FUNC>{}, a, s);
+}
+#define CHF_FOR_REGN_NS(X, F) X(F, 8) X(F, 16) X(F, 32)
+#define CHF_FOR_REGN_C(X, F, NS) X(F, 1, NS) X(F, 2, NS) X(F, 4, NS) X(F, 8, NS) X(F, 16, NS)
+#define CHF_FOR_REGN_MODE(X, F, C, NS) X(F, C, MODE_HVP, NS) X(F, C, MODE_HESS, NS) X(F, C, MODE_SYM_HVP, NS) \
+  X(F, C, MODE_SYM_HESS, NS) X(F, C, MODE_HESS_GRAD, NS)
+#define CHF_DECL_REGN2(F, C, M, NS) extern template cudaError_t launch_reg_n<F, C, M, NS>(BatchArgs, cudaStream_t);
+#define CHF_DECL_REGN1(F, C, NS) CHF_FOR_REGN_MODE(CHF_DECL_REGN2, F, C, NS)
+#define CHF_DECL_REGN0(F, NS) CHF_FOR_REGN_C(CHF_DECL_REGN1, F, NS)
+CHF_FOR_REGN_NS(CHF_DECL_REGN0, FUNC_ROSENBROCK)
+CHF_FOR_REGN_NS(CHF_DECL_REGN0, FUNC_ACKLEY)
+CHF_FOR_REGN_NS(CHF_DECL_REGN0, FUNC_PRODSUM)
 
 // NEXT-4 seed-sparse F3 HVP (f3_sparse.cuh): CB = column block, (A, B) in shared memory for
 // n <= 32, else read from the caller's params; SLIM tiles for n > 32

@@ -12,7 +12,7 @@ def test_executed_entry_current_and_stale(tmp_path):
     tab = {"src_hash": "abc", "entries": {
         "rosenbrock n=16 C=16": {"executed_flops_per_point": 0.5 * model, "model_flops_per_point": model,
                                  "fp64_pipe_active_pct": 80.0, "dram_bytes_per_launch": 1.0, "m": 1,
-                                 "kernel": "void hvp_reg_kernel<BuiltinFunc<0>, 16, 0, 4>(BatchArgs, T1)"},
+                                 "kernel": "void hvp_reg_kernel<BuiltinFunc<0>, 16, 0, 4, 16>(BatchArgs, T1)"},
         "fletcher_powell n=16 C=4 sym_hvp": {"executed_flops_per_point": 10.0, "model_flops_per_point": 20.0,
                                              "fp64_pipe_active_pct": 60.0, "dram_bytes_per_launch": 1.0, "m": 1,
                                              "kernel": "void hvp_f3_mma_kernel<16, 2>(BatchArgs)"},
@@ -30,6 +30,10 @@ def test_executed_entry_current_and_stale(tmp_path):
     assert bench.executed_entry("fletcher_powell", 16, 8, "abc", path=str(p)) is None
     assert bench.kernel_matches_path("void hvp_stream_kernel<BuiltinFunc<0>, 1, 2>(BatchArgs, T1)", "stream")
     assert not bench.kernel_matches_path("void hvp_reg_kernel<SparseFunc<0>, 1, 0, 4>(BatchArgs, T1)", "reg")
+    # the last template argument of the register kernel is NS (0: runtime n)
+    assert bench.kernel_matches_path("void hvp_reg_kernel<BuiltinFunc<0>, 16, 0, 4, 16>(BatchArgs, T1)", "reg_ns")
+    assert bench.kernel_matches_path("void hvp_reg_kernel<BuiltinFunc<0>, 4, 0, 4, 0>(BatchArgs, T1)", "reg")
+    assert not bench.kernel_matches_path("void hvp_reg_kernel<BuiltinFunc<0>, 16, 0, 4, 0>(BatchArgs, T1)", "reg_ns")
     assert bench.executed_entry("ackley", 16, 16, "abc", path=str(p)) is None
     assert bench.executed_entry("ackley", 16, 16, "abc", path=str(tmp_path / "missing.json")) is None
 

@@ -208,9 +208,10 @@ def test_kernel_path_introspection():
     assert chf.path("fletcher_powell", 100, 4, "sym_hvp") == "f3_dmma"
     assert chf.path("fletcher_powell", 16, 4, "hvp_seedsparse") == "f3_seedsparse"
     assert chf.path("rosenbrock", 2, 1) == "stream"
-    assert chf.path("rosenbrock", 16, 16) == "reg"
-    assert chf.path("ackley", 8, 1) == "reg" and chf.path("prodsum", 8, 4) == "stream"
-    assert chf.path("ackley", 4, 1) == "stream" and chf.path("rosenbrock", 8, 8) == "reg"
+    assert chf.path("rosenbrock", 16, 16) == "reg_ns" and chf.path("rosenbrock", 12, 4) == "reg"
+    assert chf.path("ackley", 8, 1) == "reg_ns" and chf.path("prodsum", 8, 4) == "stream"
+    assert chf.path("ackley", 4, 1) == "stream" and chf.path("rosenbrock", 8, 8) == "reg_ns"
+    assert chf.path("prodsum", 32, 32) == "reg_ns" and chf.path("prodsum", 64, 16) == "reg"
     assert chf.path("rosenbrock", 8, 2, "hvp_hoisted") == "small_hoisted"
     assert chf.path("rosenbrock", 3, 2) == "unsupported"
 

@@ -239,6 +239,33 @@ struct AckleyOnePass {
   }
 };
 
+// Rosenbrock with compile-time n (variable loop fully unrolled; row i and chunk cs stay
+// runtime, so the seeds are still formed per evaluation)
+template <int NS>
+struct RosenFixed {
+  static constexpr bool kTrig2Pi = false;
+  template <int C, class Seed>
+  CHF_INL hd<C> operator()(int, const Seed& y) const {
+    hd<C> s;
+    auto yc = y(1);
+    {
+      const auto y0 = y(0);
+      const auto d = hd_fnma(y0, y0, yc);
+      const auto e = 1.0 - y0;
+      s = hd_fma(e, e, 100.0 * (d * d));
+    }
+#pragma unroll
+    for (int i = 1; i < NS - 1; i++) {
+      const auto yi = yc;
+      yc = y(i + 1);
+      const auto d = hd_fnma(yi, yi, yc);
+      const auto e = 1.0 - yi;
+      s = hd_fma(e, e, hd_axpy(100.0, d * d, s));
+    }
+    return s;
+  }
+};
+
 // persistent CTAs, static tile order, the next tile's points/vectors prefetched with 8-byte
 // cp.async into the other half of a double buffer while the current tile is evaluated
 CHF_INL void cp_async8(double* dst, const double* src) {
@@ -361,6 +388,22 @@ int main(int argc, char** argv) {
     for (int64_t q = 0; q < m * n; q++) bad += ref[q] != got[q];
     printf("carry parity: %lld bitwise mismatches of %lld\n", (long long)bad, (long long)(m * n));
   }
+  auto cmp0 = [&](const char* name, auto&& la, auto&& lb) {
+    std::vector<double> ref(m * n), got(m * n);
+    la();
+    CK(cudaMemcpy(ref.data(), dout, m * n * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemset(dout, 0, m * n * 8));
+    lb();
+    CK(cudaMemcpy(got.data(), dout, m * n * 8, cudaMemcpyDeviceToHost));
+    int64_t bad = 0;
+    for (int64_t q = 0; q < m * n; q++) bad += !(ref[q] == got[q] || (ref[q] != ref[q] && got[q] != got[q]));
+    printf("%s parity: %lld bitwise mismatches of %lld\n", name, (long long)bad, (long long)(m * n));
+  };
+  timeit("fixed16", 1, [&] { CK((launch_functor<RosenFixed<16>, 16, MODE_HVP>(RosenFixed<16>{}, a, 0))); });
+  timeit("fixed16c8", 1, [&] { CK((launch_functor<RosenFixed<16>, 8, MODE_HVP>(RosenFixed<16>{}, a, 0))); });
+  timeit("lib_c8", 1, [&] { CK((launch_functor<F, 8, MODE_HVP>(F{}, a, 0))); });
+  cmp0("fixed16", [&] { CK((launch_functor<F, 16, MODE_HVP>(F{}, a, 0))); },
+       [&] { CK((launch_functor<RosenFixed<16>, 16, MODE_HVP>(RosenFixed<16>{}, a, 0))); });
   auto cmp = [&](const char* name, auto&& la, auto&& lb) {
     std::vector<double> ref(m * n), got(m * n);
     la();
