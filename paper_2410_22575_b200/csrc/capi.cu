@@ -181,10 +181,26 @@ bool stream_small_n(int func, int n, int C) {
 #ifndef CHF_REGN
 #define CHF_REGN 1  // register path: kernels compiled for n in {8, 16, 32} (0: runtime-n kernel only)
 #endif
+#ifndef CHF_REGN_BIG
+#define CHF_REGN_BIG 1  // ... and for n in {64, 128}, Alg 7
+#endif
 // Used where it measured faster (profiles/r02/ns/summary.txt: 1.1-5.8x for every HVP mode and
-// F1/F2 Hessians); prodsum's Hessian modes measured up to 1.3x slower and keep the runtime-n kernel.
-bool regn_use(int func, int n, int mode) {
-  if (!CHF_REGN || !(n == 8 || n == 16 || n == 32)) return false;
+// F1/F2 Hessians at n <= 32; prodsum's Hessian modes measured up to 1.3x slower and keep the
+// runtime-n kernel).  n in {64, 128}, Alg 7 only (profiles/r02/ns/big_summary.txt): prodsum
+// 2.4-10x at every C; Rosenbrock at kernel chunk C >= 8 (n = 64, 1.1-1.4x) / C = 16 (n = 128,
+// 1.03x); Ackley at n = 64, C >= 4 (1.2-1.6x) -- elsewhere the unrolled kernel spills.
+bool regn_use(int func, int n, int C, int mode) {
+  if (!CHF_REGN) return false;
+  if (n == 64 || n == 128) {
+    if (!CHF_REGN_BIG || mode != MODE_HVP) return false;
+    switch (func) {
+      case CHESSFAD_PRODSUM: return true;
+      case CHESSFAD_ROSENBROCK: return C >= (n == 64 ? 8 : 16);
+      case CHESSFAD_ACKLEY: return n == 64 && C >= 4;
+    }
+    return false;
+  }
+  if (!(n == 8 || n == 16 || n == 32)) return false;
   return !(func == CHESSFAD_PRODSUM && mode_hess(mode));
 }
 
@@ -216,7 +232,7 @@ cudaError_t dispatch_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s)
     }
     return dispatch_reg<MODE_HVP>(func, Capi, a, s);  // no hoisted kernel: per-evaluation path
   } else {
-    if (regn_use(func, a.n, MODE)) {  // the kernel compiled for this n (kernels.cuh NS)
+    if (regn_use(func, a.n, C, MODE)) {  // the kernel compiled for this n (kernels.cuh NS)
 #define CHF_CASE_NS(F, NS)                                     \
   if (a.n == NS) switch (C) {                                  \
       case 1: return launch_reg_n<F, 1, MODE, NS>(a, s);       \
@@ -225,6 +241,13 @@ cudaError_t dispatch_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s)
       case 8: return launch_reg_n<F, 8, MODE, NS>(a, s);       \
       case 16: return launch_reg_n<F, 16, MODE, NS>(a, s);     \
     }
+      if constexpr (MODE == MODE_HVP) {
+        switch (func) {
+          case CHESSFAD_ROSENBROCK: CHF_FOR_REGN_BIG_NS(CHF_CASE_NS, FUNC_ROSENBROCK) break;
+          case CHESSFAD_ACKLEY: CHF_CASE_NS(FUNC_ACKLEY, 64) break;
+          case CHESSFAD_PRODSUM: CHF_FOR_REGN_BIG_NS(CHF_CASE_NS, FUNC_PRODSUM) break;
+        }
+      }
       switch (func) {
         case CHESSFAD_ROSENBROCK: CHF_FOR_REGN_NS(CHF_CASE_NS, FUNC_ROSENBROCK) break;
         case CHESSFAD_ACKLEY: CHF_FOR_REGN_NS(CHF_CASE_NS, FUNC_ACKLEY) break;
@@ -634,8 +657,9 @@ const char* chessfad_path(int func, int n, int csize, int algo) {
   if (algo == CHESSFAD_ALGO_HVP && stream_small_n(func, n, C)) return "stream";  // 16-byte-aligned buffers
   if (algo == CHESSFAD_ALGO_HVP_HOISTED && (n == 2 || n == 4 || n == 8 || n == 16)) return "small_hoisted";
   const int mode = algo == CHESSFAD_ALGO_HESSIAN ? MODE_HESS : algo == CHESSFAD_ALGO_SYM_HESSIAN ? MODE_SYM_HESS
-                   : algo == CHESSFAD_ALGO_HESSIAN_GRAD ? MODE_HESS_GRAD : MODE_HVP;
-  return regn_use(func, n, mode) ? "reg_ns" : "reg";
+                   : algo == CHESSFAD_ALGO_HESSIAN_GRAD ? MODE_HESS_GRAD
+                   : algo == CHESSFAD_ALGO_SYM_HVP ? MODE_SYM_HVP : MODE_HVP;
+  return regn_use(func, n, C, mode) ? "reg_ns" : "reg";
 }
 
 const char* chessfad_version(void) { return "chessfad-b200 0.1.0 (sm_100a)"; }

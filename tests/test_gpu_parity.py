@@ -178,7 +178,9 @@ def test_edge_cases(chf):
 @pytest.mark.parametrize("family,func,n,C", [("stream", "rosenbrock", 2, 1), ("stream", "ackley", 4, 2),
                                               ("stream", "prodsum", 8, 8), ("reg", "rosenbrock", 5, 5),
                                               ("reg_ns", "ackley", 16, 16), ("reg_ns", "rosenbrock", 32, 4),
-                                              ("reg_ns", "prodsum", 16, 2), ("reg", "ackley", 12, 4), ("f3_dmma", "fletcher_powell", 16, 4),
+                                              ("reg_ns", "prodsum", 16, 2), ("reg", "ackley", 12, 4),
+                                              ("reg_ns", "prodsum", 64, 16), ("reg_ns", "rosenbrock", 128, 16),
+                                              ("reg_ns", "ackley", 64, 8), ("reg_ns", "ackley", 8, 8), ("f3_dmma", "fletcher_powell", 16, 4),
                                               ("f3_dmma", "fletcher_powell", 72, 8)])
 def test_small_m_every_family(chf, family, func, n, C):
     """Tiny and ragged batches on every kernel family: m = 1, 2, 7, 63, 65, 257 (one partial
