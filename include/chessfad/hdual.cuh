@@ -7,7 +7,7 @@
 //   v[C+2 .. 2C+1]  d2f/dx_i dx_{cs..}   (one chunk of row i of the Hessian)
 // A hDual<C> is 2C+2 doubles = 4C+4 registers; it lives in registers, never in memory.
 //
-// Two types carry it (reading R6):
+// Two types carry it (reading R7):
 //   hd<C>  every slot stored;
 //   hs<C>  "seed-shaped": slots 0 .. C+1 stored, the C second-order slots ZERO BY
 //          CONSTRUCTION.  A CHUNK-INIT seed (Alg 4: y_k = <a_k, [k==i],

@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(F3Mma<NN, MODE>::W * 32, 1) hvp_f3_mma_kernel(
             const double s0 = sB[j * TS], c0 = cB[j * TS];
             const double y1 = (j == i) ? 1.0 : 0.0, y2 = (j == col) ? 1.0 : 0.0;
             // sin: g' = cos a, g'' = -sin a;   cos: g' = -sin a, g'' = -cos a   (unary rule)
-            // slot C+2+c: g' y[C+2+c] + (g'' y1) y2, the seed's y[C+2+c] a structural zero (reading R6)
+            // slot C+2+c: g' y[C+2+c] + (g'' y1) y2, the seed's y[C+2+c] a structural zero (reading R7)
             const double xa2 = c0 * y2, xaC = ((-s0) * y1) * y2;
             const double xb2 = (-s0) * y2, xbC = ((-c0) * y1) * y2;
 #pragma unroll

@@ -86,9 +86,15 @@ CHF_FOR_SMALL(CHF_DECL_SMALL, FUNC_PRODSUM)
 
 // Alg 7 at n = NS in {2, 4, 8}: thread per point, persistent grid, bulk-copy ring
 // (stream_small.cuh).  Grid = min(tiles, SMs x resident CTAs), resident CTAs queried once.
+// compile-time chunk start (reading R8) where the kernel is FP64-bound; the HBM-bound corners
+// (Rosenbrock / prodsum at n = 2, prodsum at n = 4) measured faster with it read per evaluation
+// (profiles/r02/stream_fold/summary.txt)
+constexpr bool stream_fold_cs(int FUNC, int NS) {
+  return !((NS == 2 && FUNC != FUNC_ACKLEY) || (NS == 4 && FUNC == FUNC_PRODSUM));
+}
 template <int FUNC, int C, int NS>
 cudaError_t launch_stream(BatchArgs a, cudaStream_t s) {
-  auto kern = hvp_stream_kernel<BuiltinFunc<FUNC>, C, NS>;
+  auto kern = hvp_stream_kernel<BuiltinFunc<FUNC>, C, NS, stream_fold_cs(FUNC, NS)>;
   constexpr size_t smem = StreamCfg<NS>::kSmem;
   static int occ = 0;
   cudaError_t e;

@@ -15,16 +15,17 @@
 //   * each thread reads its point and vector as 16-byte words, keeps them in registers, and
 //     writes its n results with 16-byte coalesced stores.
 //
-// Per-evaluation execution.  The row / chunk / variable loops are unrolled (NS is a
-// compile-time constant, so the point, vector and result live in registers), but every
-// evaluation reads its row index and chunk start (from a per-CTA table) and the point's
-// coordinates (from the thread's own shared-memory copy) with VOLATILE shared loads: to both
-// compilers (NVVM and ptxas) they are fresh runtime values in each evaluation, exactly as in
-// the runtime-n kernel, so the CHUNK-INIT seeds stay runtime 0/1 values and the value channel
-// is recomputed in every evaluation -- no folding or sharing of work across evaluations (that
-// is the separate NEXT-4 hoisted entry point).  (Register moves through inline asm are not
-// enough: ptxas propagates them, folds the seeds and shares the evaluations -- measured, same
-// SASS for C = 1 and C = 2 at n = 2.)
+// Per-evaluation execution (reading R8).  The row / chunk / variable loops are
+// unrolled (NS is a compile-time constant, so the point, vector and result live in registers),
+// but every evaluation reads its row index (from a per-CTA table) and the point's coordinates
+// (from the thread's own shared-memory copy) with VOLATILE shared loads: to both compilers
+// (NVVM and ptxas) they are fresh runtime values in each evaluation, so the value channel is
+// recomputed in every evaluation and no work is shared across evaluations (that is the
+// separate NEXT-4 hoisted entry point).  The chunk start j*C is a compile-time constant, as in
+// the paper's NV/CHUNK-templated kernels: the seed's chunk slots are constants within the
+// evaluation and nvcc folds them (x*1 -> x, IEEE-exact).  (Register moves through inline asm
+// do not keep values opaque: ptxas propagates them, folds the seeds and shares the
+// evaluations -- measured, same SASS for C = 1 and C = 2 at n = 2.)
 #pragma once
 #include <cstdint>
 
@@ -106,7 +107,9 @@ struct StreamCfg {
   static constexpr size_t kSmem = 2 * kStages * kTileBytes + kTileBytes + 8 * kEvals + 8 * kStages + 16;
 };
 
-template <class F, int C, int NS>
+// KCS: the chunk start is a compile-time constant (true) or read per evaluation like the row
+// index (false; the HBM-bound corners measured faster that way, launch.cuh stream_fold_cs)
+template <class F, int C, int NS, bool KCS = true>
 __global__ void __launch_bounds__(kStreamTP, NS == 8 ? 1 : 2) hvp_stream_kernel(BatchArgs p, F f) {
   static_assert(NS % 2 == 0 && NS % C == 0, "NS even, C | NS");
   using Cfg = StreamCfg<NS>;
@@ -187,8 +190,10 @@ __global__ void __launch_bounds__(kStreamTP, NS == 8 ? 1 : 2) hvp_stream_kernel(
         double ao[NS];
 #pragma unroll
         for (int k = 0; k < NS; k++) ao[k] = ld_vol(acopy + k * kStreamTP + tid);
-        const int2 ic = ld_vol(evtab + i * (NS / C) + j);  // == (i, j C), opaque
-        const RegSeed<C> y{ao, 1, ic.x, ic.y, ts, tc};
+        // row i opaque (read per evaluation), chunk start j C a compile-time constant: the seed's
+        // chunk slots fold within the evaluation (reading R8), nothing is shared across evaluations
+        const int2 ic = ld_vol(evtab + i * (NS / C) + j);  // == (i, j C)
+        const RegSeed<C> y{ao, 1, ic.x, KCS ? j * C : ic.y, ts, tc};
         const hd<C> t = f.template operator()<C>(NS, y);  // CHUNK-INIT + f<hDual<C>>, Alg 7 :389-390
 #pragma unroll
         for (int l = 0; l < C; l++) res = res + t.v[C + 2 + l] * v[j * C + l];  // :392-394
