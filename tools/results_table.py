@@ -28,7 +28,7 @@ def main(d):
             k = (r["n"], r["algo"], r["func"], r["m"])
             if k not in best or r["ms"] < best[k]["ms"]:
                 best[k] = r
-    print("| n | algorithm | function | best C | m | points/s | ms | executed FP64 (of 37.2 TF/s) | exec/model | FP64 pipe |")
+    print("| n | algorithm | function | best C | m | points/s | ms | executed FP64 (of 37.2 TF/s) | exec/model | pipe busy |")
     print("|---|---|---|---|---|---|---|---|---|---|")
     for k in sorted(best):
         r = best[k]
@@ -39,7 +39,8 @@ def main(d):
             ef = e["executed_flops_per_point"] * r["m"] / (r["ms"] * 1e-3)
             ex = f"{ef / PEAK:.2f}"
             ratio = f"{e['executed_flops_per_point'] / e['model_flops_per_point']:.3f}"
-            pipe = f"{e['fp64_pipe_active_pct']:.0f}%"
+            dm = e.get("dmma_pipe_active_pct") or 0.0
+            pipe = f"DMMA {dm:.0f}%" if dm > e["fp64_pipe_active_pct"] else f"{e['fp64_pipe_active_pct']:.0f}%"
         print(f"| {r['n']} | {r['algo']} | {r['func']} | {r['C']} | {r['m']} | {r['points_per_s']:.3g} | "
               f"{r['ms']:.3f} | {ex} | {ratio} | {pipe} |")
 
