@@ -151,6 +151,9 @@ CHF_INL RowSink<MODE> make_sink(const BatchArgs& p, int i, int64_t e, const doub
 }
 
 // ---------------------------------------------------------------- F1, F2, F4: hDual<C> in registers
+#ifndef CHF_NS_CHUNK_UNROLL
+#define CHF_NS_CHUNK_UNROLL 4  // compiled-n kernels: unroll the chunk loop up to this many chunks
+#endif
 #ifndef CHF_REG_MINB
 #define CHF_REG_MINB 1  // min CTAs/SM hint of the register path (tuning experiments)
 #endif
@@ -192,15 +195,22 @@ __global__ void __launch_bounds__(W * 32, CHF_REG_MINB) hvp_reg_kernel(BatchArgs
   const double* tcos = TRIG ? s_cos + g * n * kPad + lane : nullptr;
   const int64_t e = e0 + g * 32 + lane;
   const int nchunk = n / C;
+  // NS > 0 with 2 .. CHF_NS_CHUNK_UNROLL chunks per row: the chunk loop unrolls too, so the chunk
+  // start is a constant in each copy (reading R8) and the seeds read the point with volatile
+  // loads (no work shared between the copies); otherwise chunks stay a runtime loop
+  // (functors that opt in with kVolSeeds = true: measured per function, profiles/r02/ns3/)
+  constexpr bool kVolOk = NS > 0 && uses_vol_seeds<F>::value;
+  constexpr int kChunkUnroll = (kVolOk && NS / C <= CHF_NS_CHUNK_UNROLL) ? (NS > 0 ? NS / C : 1) : 1;
+  constexpr bool kVolSeed = kVolOk && (kChunkUnroll > 1 || NS >= 32);
   for (int i = warp / G; i < n; i += rstep) {
     const int scn = i / Capi;  // row i's first chunk (symmetric modes)
     RowSink<MODE> sink = make_sink<MODE>(p, i, e, v, o);
     double gi = 0.0;  // MODE_HESS_GRAD: df/dx_i (slot v[1], identical for every chunk of row i)
-#pragma unroll 1
+#pragma unroll kChunkUnroll
     for (int j = mode_sym(MODE) ? (scn * Capi) / C : 0; j < nchunk; j++) {
       const int cs = j * C;
       sink.mirror = cs / Capi > scn;
-      const LaneSeed<C, (NS > 0)> y{a, kPad, i, cs, tsin, tcos};
+      const LaneSeed<C, (NS > 0), kVolSeed> y{a, kPad, i, cs, tsin, tcos};
       const hd<C> t = f.template operator()<C>(n, y);  // CHUNK-INIT + f<hDual<C>>, Alg 7 :389-390
 #pragma unroll
       for (int l = 0; l < C; l++) sink(cs + l, t.v[C + 2 + l]);  // :392-394 / :210-212 / :417-421

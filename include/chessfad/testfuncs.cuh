@@ -17,13 +17,24 @@ namespace chessfad {
 
 enum { FUNC_ROSENBROCK = 0, FUNC_ACKLEY = 1, FUNC_FLETCHER_POWELL = 2, FUNC_PRODSUM = 3 };
 
+// shared-memory load neither compiler may merge, hoist or fold (a fresh value per call)
+CHF_INL double ld_shared_volatile(const double* p) {
+  double r;
+  asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(r) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return r;
+}
+
 // CHUNK-INIT seed for the lane's own point; row i and chunk start cs are warp-uniform.
 //   y[k] = < a_k, [k==i], e_{k-cs} if cs <= k < cs+C, 0 ... 0 >          (Alg 4)
 // STATIC: n is a compile-time constant of the kernel (the paper's NV template, Fig. 2,
 // PAPER.md:485-499) and the functions' variable loops are fully unrolled, so k is a constant
 // in each copy; row i and chunk start cs stay runtime values (every evaluation is formed and
 // executed on its own, as in Alg 7).
-template <int C, bool STATIC = false>
+// VOL (STATIC only): a_k (and Ackley's tables) are read with volatile loads, so each evaluation
+// reads its own copy and no compiler can share work between evaluations whose code sits side by
+// side (the unrolled chunk loop of kernels.cuh); it also keeps nvcc from hoisting every
+// coordinate load of the unrolled variable loop (register pressure at n >= 32)
+template <int C, bool STATIC = false, bool VOL = false>
 struct LaneSeed {
   static constexpr bool kStatic = STATIC;  // false: runtime n, loops keep their partial unrolling
   static constexpr bool kFused = true;    // fused accumulate forms (R5) in the running sums
@@ -36,13 +47,16 @@ struct LaneSeed {
   const double* cos2pi;
   CHF_INL hs<C> operator()(int k) const {
     hs<C> y;
-    y.v[0] = a[k * stride];
+    y.v[0] = VOL ? ld_shared_volatile(a + k * stride) : a[k * stride];
     y.v[1] = (k == i) ? 1.0 : 0.0;
     const int off = k - cs;
 #pragma unroll
     for (int l = 0; l < C; l++) y.v[2 + l] = (off == l) ? 1.0 : 0.0;
     return y;  // second-order slots: structural zeros (hdual.cuh hs<C>)
   }
+  // Ackley's tabulated sin / cos(2 pi a_k) (volatile with VOL, as a_k above)
+  CHF_INL double s2pi(int k) const { return VOL ? ld_shared_volatile(sin2pi + k * stride) : sin2pi[k * stride]; }
+  CHF_INL double c2pi(int k) const { return VOL ? ld_shared_volatile(cos2pi + k * stride) : cos2pi[k * stride]; }
 };
 
 // Compile-time-n seed (small-n path, kernels.cuh hvp_small_kernel): the point lives in
@@ -69,6 +83,8 @@ struct StaticSeed {
     for (int l = 0; l < C; l++) y.v[2 + l] = (k - cs == l) ? 1.0 : 0.0;
     return y;
   }
+  CHF_INL double s2pi(int k) const { return sin2pi[k * stride]; }
+  CHF_INL double c2pi(int k) const { return cos2pi[k * stride]; }
 };
 
 #ifndef CHF_SUM_UNROLL
@@ -152,14 +168,14 @@ CHF_INL hd<C> f_ackley(int n, const Seed& y) {
   // bit-identical to the tabulated argument (same single rounding of two_pi * a_i)
   auto cos2pi = [&](int k) {
     const auto u = two_pi * y(k);
-    const double s = y.sin2pi[k * y.stride], c = y.cos2pi[k * y.stride];
+    const double s = y.s2pi(k), c = y.c2pi(k);
     return hd_unary(u, c, -s, -c);
   };
   hd<C> s2 = cos2pi(0);
   seed_loop<Seed, 0>(1, n, [&](int i) {
     if constexpr (Seed::kFused) {  // s2 + cos(2 pi y_i), fused (R5)
       const auto u = two_pi * y(i);
-      s2 = hd_unary_acc(u, y.cos2pi[i * y.stride], -y.sin2pi[i * y.stride], -y.cos2pi[i * y.stride], s2);
+      s2 = hd_unary_acc(u, y.c2pi(i), -y.s2pi(i), -y.c2pi(i), s2);
     } else {
       s2 = s2 + cos2pi(i);
     }
@@ -197,6 +213,9 @@ CHF_INL hd<C> eval_f(int n, const Seed& y) {
 template <int FUNC>
 struct BuiltinFunc {
   static constexpr bool kTrig2Pi = FUNC == FUNC_ACKLEY;
+  // compiled-n kernels: volatile seed loads + unrolled chunk loop (kernels.cuh); measured
+  // faster for Rosenbrock at every n, slower for prodsum and mixed for Ackley (profiles/r02/ns3/)
+  static constexpr bool kVolSeeds = FUNC == FUNC_ROSENBROCK;
   template <int C, class Seed>
   CHF_INL hd<C> operator()(int n, const Seed& y) const {
     return eval_f<FUNC, C>(n, y);
@@ -268,15 +287,15 @@ CHF_INL hd<C> fsp_ackley(int n, const LaneSeed<C>& y) {
     const auto yk = y(k);
     s1 = hd_fma(yk, yk, s1);
     const auto u = two_pi * yk;
-    s2 = hd_unary_acc(u, y.cos2pi[k * y.stride], -y.sin2pi[k * y.stride], -y.cos2pi[k * y.stride], s2);
+    s2 = hd_unary_acc(u, y.c2pi(k), -y.s2pi(k), -y.c2pi(k), s2);
   });
   {  // value slots: the chains of f_ackley (first term initialises)
     const double a0 = y.a[0];
-    double v1 = a0 * a0, v2 = y.cos2pi[0];
+    double v1 = a0 * a0, v2 = y.c2pi(0);
     for (int k = 1; k < n; k++) {
       const double ak = y.a[k * y.stride];
       v1 = __fma_rn(ak, ak, v1);
-      v2 = v2 + y.cos2pi[k * y.stride];
+      v2 = v2 + y.c2pi(k);
     }
     s1.v[0] = v1;
     s2.v[0] = v2;
@@ -296,6 +315,15 @@ struct SparseFunc {
     else if constexpr (FUNC == FUNC_ACKLEY) return fsp_ackley<C>(n, y);
     else return fsp_prodsum<C>(n, y);
   }
+};
+
+template <class F, class = void>
+struct uses_vol_seeds {
+  static constexpr bool value = false;
+};
+template <class F>
+struct uses_vol_seeds<F, decltype((void)F::kVolSeeds)> {
+  static constexpr bool value = F::kVolSeeds;
 };
 
 template <class F, class = void>

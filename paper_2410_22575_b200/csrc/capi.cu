@@ -186,16 +186,24 @@ bool stream_small_n(int func, int n, int C) {
 #endif
 // Used where it measured faster (profiles/r02/ns/summary.txt: 1.1-5.8x for every HVP mode and
 // F1/F2 Hessians at n <= 32; prodsum's Hessian modes measured up to 1.3x slower and keep the
-// runtime-n kernel).  n in {64, 128}, Alg 7 only (profiles/r02/ns/big_summary.txt): prodsum
-// 2.4-10x at every C; Rosenbrock at kernel chunk C >= 8 (n = 64, 1.1-1.4x) / C = 16 (n = 128,
-// 1.03x); Ackley at n = 64, C >= 4 (1.2-1.6x) -- elsewhere the unrolled kernel spills.
+// runtime-n kernel).  n in {64, 128}, Alg 7 only (profiles/r02/ns/big_summary.txt,
+// profiles/r02/ns3/summary.txt): prodsum 2.4-10x at every C; Rosenbrock (volatile seeds,
+// unrolled chunks) at n = 64 every C (1.04-3.1x), at n = 128 C >= 4 (C = 1, 2 slower); Ackley
+// at n = 64, C >= 4 (1.2-1.6x) -- elsewhere the unrolled kernel spills.
+#ifndef CHF_REGN_ALL
+#define CHF_REGN_ALL 0  // tuning: every compiled-n instantiation, measured or not
+#endif
 bool regn_use(int func, int n, int C, int mode) {
   if (!CHF_REGN) return false;
+  if (CHF_REGN_ALL) {
+    if (n == 64 || n == 128) return mode == MODE_HVP && !(func == CHESSFAD_ACKLEY && n == 128);
+    return n == 8 || n == 16 || n == 32;
+  }
   if (n == 64 || n == 128) {
     if (!CHF_REGN_BIG || mode != MODE_HVP) return false;
     switch (func) {
       case CHESSFAD_PRODSUM: return true;
-      case CHESSFAD_ROSENBROCK: return C >= (n == 64 ? 8 : 16);
+      case CHESSFAD_ROSENBROCK: return n == 64 || C >= 4;
       case CHESSFAD_ACKLEY: return n == 64 && C >= 4;
     }
     return false;

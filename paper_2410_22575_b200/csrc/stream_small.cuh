@@ -65,6 +65,8 @@ struct RegSeed {
     for (int l = 0; l < C; l++) y.v[2 + l] = (off == l) ? 1.0 : 0.0;
     return y;
   }
+  CHF_INL double s2pi(int k) const { return sin2pi[k]; }
+  CHF_INL double c2pi(int k) const { return cos2pi[k]; }
 };
 
 // ---------------------------------------------------------------- mbarrier / bulk copy PTX

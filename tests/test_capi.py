@@ -213,7 +213,7 @@ def test_kernel_path_introspection():
     assert chf.path("ackley", 4, 1) == "stream" and chf.path("rosenbrock", 8, 8) == "reg_ns"
     assert chf.path("prodsum", 32, 32) == "reg_ns" and chf.path("prodsum", 64, 16) == "reg_ns"
     assert chf.path("prodsum", 32, 4, "hessian") == "reg" and chf.path("rosenbrock", 32, 4, "hessian") == "reg_ns"
-    assert chf.path("rosenbrock", 64, 4) == "reg" and chf.path("rosenbrock", 64, 8) == "reg_ns"
+    assert chf.path("rosenbrock", 128, 2) == "reg" and chf.path("rosenbrock", 64, 1) == "reg_ns"
     assert chf.path("ackley", 128, 16) == "reg" and chf.path("ackley", 64, 64) == "reg_ns"
     assert chf.path("rosenbrock", 64, 16, "sym_hvp") == "reg" and chf.path("rosenbrock", 16, 16, "sym_hvp") == "reg_ns"
     assert chf.path("rosenbrock", 8, 2, "hvp_hoisted") == "small_hoisted"

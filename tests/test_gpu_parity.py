@@ -89,14 +89,14 @@ def test_large_n(chf, func):
         P, V = synth.points(2, n, m), synth.vectors(2, n, m)
         params = _params(func, n)
         ref, sabs = oracle.hvp_batch(func, P, V, n if n <= 32 else 32, params)
-        for C in [1, 8, 32, 64, n]:
+        for C in [1, 2, 4, 8, 16, 32, 64, n]:
             if chf.is_supported(func, n, C):
                 _check(_gpu_hvp(chf, func, P, V, C, params), ref, sabs)
 
 
 # ------------------------------------------------------------ bit-exact integer pin
 @pytest.mark.parametrize("func", ["rosenbrock", "prodsum"])
-@pytest.mark.parametrize("n", [2, 4, 8, 16])
+@pytest.mark.parametrize("n", [2, 4, 8, 16, 32, 64])
 def test_integer_inputs_bitwise(chf, func, n):
     """Integer points/vectors in {-9..9}: every intermediate is an exact integer, so the GPU
     must equal the exact rational closed form bit for bit under any FMA/reduction order."""
@@ -180,7 +180,8 @@ def test_edge_cases(chf):
                                               ("reg_ns", "ackley", 16, 16), ("reg_ns", "rosenbrock", 32, 4),
                                               ("reg_ns", "prodsum", 16, 2), ("reg", "ackley", 12, 4),
                                               ("reg_ns", "prodsum", 64, 16), ("reg_ns", "rosenbrock", 128, 16),
-                                              ("reg_ns", "ackley", 64, 8), ("reg_ns", "ackley", 8, 8), ("f3_dmma", "fletcher_powell", 16, 4),
+                                              ("reg_ns", "ackley", 64, 8), ("reg_ns", "ackley", 8, 8),
+                                              ("reg_ns", "rosenbrock", 16, 4), ("reg_ns", "rosenbrock", 64, 2), ("f3_dmma", "fletcher_powell", 16, 4),
                                               ("f3_dmma", "fletcher_powell", 72, 8)])
 def test_small_m_every_family(chf, family, func, n, C):
     """Tiny and ragged batches on every kernel family: m = 1, 2, 7, 63, 65, 257 (one partial
