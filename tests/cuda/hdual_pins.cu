@@ -4,6 +4,8 @@
 // tests/test_gpu_hdual_pins.py with nvcc into a small .so; nothing here is product code.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "chessfad/testfuncs.cuh"
 
 using namespace chessfad;
@@ -44,6 +46,66 @@ __global__ void op_kernel(int op, const double* u_, const double* v_, double c, 
     case OP_GE: r.v[0] = (u >= v) ? 1.0 : 0.0; break;
   }
   for (int s = 0; s < hd<C>::N; s++) out[s] = r.v[s];
+}
+
+// Reading R7: every rule with seed-shaped operands (hs<C>: second-order slots
+// structural zeros) against the same rule on the operands converted to full hd<C>.  Mode bits:
+// 1 = u seed-shaped, 2 = v seed-shaped, 4 = acc seed-shaped.  out[0..N) typed, out[N..2N) full.
+enum { SS_ADD, SS_SUB, SS_MUL, SS_DIV, SS_FMA, SS_FNMA, SS_AXPY, SS_SIN, SS_EXP, SS_SQRT, SS_UACC, SS_SMUL, SS_CSUB };
+template <int C, class U, class V, class A>
+__device__ void ss_apply(int op, const U& u, const V& v, const A& acc, double c, double* out) {
+  hd<C> r;
+  switch (op) {
+    case SS_ADD: r = u + v; break;
+    case SS_SUB: r = u - v; break;
+    case SS_MUL: r = u * v; break;
+    case SS_DIV: r = u / v; break;
+    case SS_FMA: r = hd_fma(u, v, acc); break;
+    case SS_FNMA: r = hd_fnma(u, v, acc); break;
+    case SS_AXPY: r = hd_axpy(c, u, acc); break;
+    case SS_SIN: r = sin(u); break;
+    case SS_EXP: r = exp(u); break;
+    case SS_SQRT: r = sqrt(u); break;
+    case SS_UACC: r = hd_unary_acc(u, 0.3, -0.7, 1.9, acc); break;
+    case SS_SMUL: r = c * u; break;
+    case SS_CSUB: r = c - u; break;
+  }
+  for (int q = 0; q < hd<C>::N; q++) out[q] = r.v[q];
+}
+template <int C, bool SU, bool SV, bool SA>
+__device__ void ss_run(int op, const double* u_, const double* v_, const double* a_, double c, double* out) {
+  using U = std::conditional_t<SU, hs<C>, hd<C>>;
+  using V = std::conditional_t<SV, hs<C>, hd<C>>;
+  using A = std::conditional_t<SA, hs<C>, hd<C>>;
+  U u;
+  V v;
+  A a;
+  hd<C> fu, fv, fa;
+  for (int q = 0; q < hd<C>::N; q++) {
+    const bool second = q >= C + 2;
+    fu.v[q] = (SU && second) ? 0.0 : u_[q];
+    fv.v[q] = (SV && second) ? 0.0 : v_[q];
+    fa.v[q] = (SA && second) ? 0.0 : a_[q];
+    if (q < U::N) u.v[q] = u_[q];
+    if (q < V::N) v.v[q] = v_[q];
+    if (q < A::N) a.v[q] = a_[q];
+  }
+  ss_apply<C>(op, u, v, a, c, out);
+  ss_apply<C>(op, fu, fv, fa, c, out + hd<C>::N);
+}
+template <int C>
+__global__ void seedshape_kernel(int op, int mode, const double* u, const double* v, const double* a, double c,
+                                 double* out) {
+  switch (mode) {
+    case 0: ss_run<C, false, false, false>(op, u, v, a, c, out); break;
+    case 1: ss_run<C, true, false, false>(op, u, v, a, c, out); break;
+    case 2: ss_run<C, false, true, false>(op, u, v, a, c, out); break;
+    case 3: ss_run<C, true, true, false>(op, u, v, a, c, out); break;
+    case 4: ss_run<C, false, false, true>(op, u, v, a, c, out); break;
+    case 5: ss_run<C, true, false, true>(op, u, v, a, c, out); break;
+    case 6: ss_run<C, false, true, true>(op, u, v, a, c, out); break;
+    case 7: ss_run<C, true, true, true>(op, u, v, a, c, out); break;
+  }
 }
 
 // CHUNK-INIT seeds of all n variables (Alg 4) from the device seed generator
@@ -101,4 +163,24 @@ extern "C" int dev_chunk_init(int n, int C, const double* a, int i, int cs, doub
     return run([](double* x, double*, double* o) { seed_kernel<2><<<1, 1>>>(s_n, x, s_i, s_cs, o); }, a, nullptr, n,
                out, n * 6);
   return 2;
+}
+
+// three operands of 2C+2 slots each packed in `in` (u | v | acc); out: typed | full
+extern "C" int dev_seedshape(int op, int mode, int C, const double* in, double c, double* out) {
+  static int s_op, s_mode;
+  static double s_c;
+  s_op = op;
+  s_mode = mode;
+  s_c = c;
+  double* d;
+  if (cudaMalloc(&d, 256 * sizeof(double))) return 1;
+  const int N = 2 * C + 2;
+  cudaMemcpy(d, in, 3 * N * sizeof(double), cudaMemcpyHostToDevice);
+  if (C == 2) seedshape_kernel<2><<<1, 1>>>(s_op, s_mode, d, d + N, d + 2 * N, s_c, d + 3 * N);
+  else if (C == 4) seedshape_kernel<4><<<1, 1>>>(s_op, s_mode, d, d + N, d + 2 * N, s_c, d + 3 * N);
+  else return 2;
+  const int err = cudaDeviceSynchronize() != cudaSuccess;
+  cudaMemcpy(out, d + 3 * N, 2 * N * sizeof(double), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return err;
 }

@@ -37,6 +37,7 @@ def lib():
     P = ctypes.POINTER(ctypes.c_double)
     lib.dev_hd_op.argtypes = [ctypes.c_int, ctypes.c_int, P, P, ctypes.c_double, P]
     lib.dev_chunk_init.argtypes = [ctypes.c_int, ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P]
+    lib.dev_seedshape.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_double, P]
     return lib
 
 
@@ -117,3 +118,23 @@ def test_device_rules_equal_oracle(lib, name):
                                    else v, c=c)
         scale = np.abs(ref).max() + 1.0
         assert np.max(np.abs(got - ref)) <= 4 * np.finfo(float).eps * scale * 8, (name, got, ref)
+
+
+def test_seed_shaped_rules_equal_full(lib):
+    """Reading R7: every rule with seed-shaped operands (second-order slots structural zeros,
+    the terms with them omitted) equals the same rule on the operands with those zeros stored,
+    bit for bit on finite inputs (up to the sign of a zero), for every mix of operand types."""
+    rng = np.random.default_rng(11)
+    names = ["add", "sub", "mul", "div", "fma", "fnma", "axpy", "sin", "exp", "sqrt", "uacc", "smul", "csub"]
+    for C in (2, 4):
+        N = 2 * C + 2
+        for k, name in enumerate(names):
+            for mode in range(8):
+                for _ in range(5):
+                    ops = rng.uniform(0.5, 2.0, 3 * N)
+                    ops[rng.random(3 * N) < 0.3] = 0.0  # exact zeros in the stored slots too
+                    ops[0] = rng.uniform(0.5, 2.0)       # u0 > 0 (sqrt, division)
+                    ops[N] = rng.uniform(0.5, 2.0)       # v0 > 0
+                    out = np.zeros(2 * N)
+                    assert lib.dev_seedshape(k, mode, C, _p(ops), 0.75, _p(out)) == 0
+                    assert np.array_equal(out[:N], out[N:]), (name, mode, C, out[:N], out[N:])
