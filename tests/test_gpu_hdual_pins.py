@@ -123,7 +123,11 @@ def test_device_rules_equal_oracle(lib, name):
 def test_seed_shaped_rules_equal_full(lib):
     """Reading R7: every rule with seed-shaped operands (second-order slots structural zeros,
     the terms with them omitted) equals the same rule on the operands with those zeros stored,
-    bit for bit on finite inputs (up to the sign of a zero), for every mix of operand types."""
+    for every mix of operand types: bit for bit (up to the sign of a zero) where the rule fixes
+    its association with explicit FMAs (the fused forms and the componentwise rules); within
+    the rounding of nvcc's contraction where it leaves the expression to it (hh*, quotient,
+    unary chain rule: a dropped zero term can change which pair nvcc contracts)."""
+    exact = {"add", "sub", "fma", "fnma", "axpy", "uacc", "smul", "csub"}
     rng = np.random.default_rng(11)
     names = ["add", "sub", "mul", "div", "fma", "fnma", "axpy", "sin", "exp", "sqrt", "uacc", "smul", "csub"]
     for C in (2, 4):
@@ -137,4 +141,8 @@ def test_seed_shaped_rules_equal_full(lib):
                     ops[N] = rng.uniform(0.5, 2.0)       # v0 > 0
                     out = np.zeros(2 * N)
                     assert lib.dev_seedshape(k, mode, C, _p(ops), 0.75, _p(out)) == 0
-                    assert np.array_equal(out[:N], out[N:]), (name, mode, C, out[:N], out[N:])
+                    if name in exact:
+                        assert np.array_equal(out[:N], out[N:]), (name, mode, C, out[:N], out[N:])
+                    else:
+                        scale = np.abs(out[N:]).max() + 1.0
+                        assert np.abs(out[:N] - out[N:]).max() <= 4 * np.finfo(float).eps * scale, (name, mode, C)
