@@ -198,8 +198,8 @@ __global__ void __launch_bounds__(W * 32, CHF_REG_MINB) hvp_reg_kernel(BatchArgs
   // NS > 0 with 2 .. CHF_NS_CHUNK_UNROLL chunks per row: the chunk loop unrolls too, so the chunk
   // start is a constant in each copy (reading R8) and the seeds read the point with volatile
   // loads (no work shared between the copies); otherwise chunks stay a runtime loop
-  // (functors that opt in with kVolSeeds = true: measured per function, profiles/r02/ns3/)
-  constexpr bool kVolOk = NS > 0 && uses_vol_seeds<F>::value;
+  // (where the functor opts in, F::vol_seeds: measured per function, profiles/r02/ns3/)
+  constexpr bool kVolOk = NS > 0 && vol_seeds_of<F>::get(NS, C, MODE);
   constexpr int kChunkUnroll = (kVolOk && NS / C <= CHF_NS_CHUNK_UNROLL) ? (NS > 0 ? NS / C : 1) : 1;
   constexpr bool kVolSeed = kVolOk && (kChunkUnroll > 1 || NS >= 32);
   for (int i = warp / G; i < n; i += rstep) {

@@ -213,9 +213,15 @@ CHF_INL hd<C> eval_f(int n, const Seed& y) {
 template <int FUNC>
 struct BuiltinFunc {
   static constexpr bool kTrig2Pi = FUNC == FUNC_ACKLEY;
-  // compiled-n kernels: volatile seed loads + unrolled chunk loop (kernels.cuh); measured
-  // faster for Rosenbrock at every n, slower for prodsum and mixed for Ackley (profiles/r02/ns3/)
-  static constexpr bool kVolSeeds = FUNC == FUNC_ROSENBROCK;
+  // compiled-n kernels (kernels.cuh NS): volatile seed loads + unrolled chunk loop for this
+  // (n, kernel chunk C, mode)?  Measured (profiles/r02/ns3/summary.txt): faster for Rosenbrock
+  // everywhere; for Ackley in the non-symmetric modes at n >= 32 with C >= 16 (n = 32 HVP 1.33x,
+  // Hessian 1.25x; n = 64 also C <= 2); slower for prodsum.
+  __host__ __device__ static constexpr bool vol_seeds(int ns, int c, int mode) {
+    return FUNC == FUNC_ROSENBROCK ||
+           (FUNC == FUNC_ACKLEY && ns >= 32 && (c >= 16 || (ns == 64 && c <= 2)) &&
+            mode != 2 && mode != 3);  // not MODE_SYM_HVP / MODE_SYM_HESS (kernels.cuh)
+  }
   template <int C, class Seed>
   CHF_INL hd<C> operator()(int n, const Seed& y) const {
     return eval_f<FUNC, C>(n, y);
@@ -317,13 +323,14 @@ struct SparseFunc {
   }
 };
 
+// F::vol_seeds(ns, c, mode) if the functor declares it, else false (user functors)
 template <class F, class = void>
-struct uses_vol_seeds {
-  static constexpr bool value = false;
+struct vol_seeds_of {
+  __host__ __device__ static constexpr bool get(int, int, int) { return false; }
 };
 template <class F>
-struct uses_vol_seeds<F, decltype((void)F::kVolSeeds)> {
-  static constexpr bool value = F::kVolSeeds;
+struct vol_seeds_of<F, decltype((void)F::vol_seeds(0, 0, 0))> {
+  __host__ __device__ static constexpr bool get(int ns, int c, int mode) { return F::vol_seeds(ns, c, mode); }
 };
 
 template <class F, class = void>

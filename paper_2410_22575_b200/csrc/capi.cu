@@ -189,7 +189,7 @@ bool stream_small_n(int func, int n, int C) {
 // runtime-n kernel).  n in {64, 128}, Alg 7 only (profiles/r02/ns/big_summary.txt,
 // profiles/r02/ns3/summary.txt): prodsum 2.4-10x at every C; Rosenbrock (volatile seeds,
 // unrolled chunks) at n = 64 every C (1.04-3.1x), at n = 128 C >= 4 (C = 1, 2 slower); Ackley
-// at n = 64, C >= 4 (1.2-1.6x) -- elsewhere the unrolled kernel spills.
+// at n = 64 every C (1.1-1.6x; volatile seeds at C <= 2 and C >= 16) -- n = 128 spills.
 #ifndef CHF_REGN_ALL
 #define CHF_REGN_ALL 0  // tuning: every compiled-n instantiation, measured or not
 #endif
@@ -204,7 +204,7 @@ bool regn_use(int func, int n, int C, int mode) {
     switch (func) {
       case CHESSFAD_PRODSUM: return true;
       case CHESSFAD_ROSENBROCK: return n == 64 || C >= 4;
-      case CHESSFAD_ACKLEY: return n == 64 && C >= 4;
+      case CHESSFAD_ACKLEY: return n == 64;
     }
     return false;
   }
