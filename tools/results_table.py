@@ -2,7 +2,8 @@
 (time_*.jsonl of tools/sweep_bench.py) joined with the ncu executed-FLOP table of the same
 build (executed_flops.json): the DESIGN.md §10 results table.
 
-    python tools/results_table.py gpurun_out/r02f3
+    python tools/results_table.py DIR [DIR2 ...]   (a later directory's sweep rows replace the
+                                                  earlier ones per (n, algorithm, function, m, C))
 """
 import glob
 import json
@@ -12,22 +13,26 @@ import sys
 PEAK = 148 * 64 * 2 * 1.965e9  # FP64 FLOP/s
 
 
-def main(d):
+def main(dirs):
     tab = {}
-    try:
-        tab = json.load(open(os.path.join(d, "executed_flops.json")))["entries"]
-    except Exception:
-        pass
+    rows = {}
+    for d in dirs:
+        try:
+            tab.update(json.load(open(os.path.join(d, "executed_flops.json")))["entries"])
+        except Exception:
+            pass
+        for f in sorted(glob.glob(os.path.join(d, "time_*.jsonl"))):
+            for line in open(f):
+                try:
+                    r = json.loads(line)
+                except Exception:
+                    continue
+                rows[(r["n"], r["algo"], r["func"], r["m"], r["C"])] = r
     best = {}
-    for f in sorted(glob.glob(os.path.join(d, "time_*.jsonl"))):
-        for line in open(f):
-            try:
-                r = json.loads(line)
-            except Exception:
-                continue
-            k = (r["n"], r["algo"], r["func"], r["m"])
-            if k not in best or r["ms"] < best[k]["ms"]:
-                best[k] = r
+    for r in rows.values():
+        k = (r["n"], r["algo"], r["func"], r["m"])
+        if k not in best or r["ms"] < best[k]["ms"]:
+            best[k] = r
     print("| n | algorithm | function | best C | m | points/s | ms | executed FP64 (of 37.2 TF/s) | exec/model | pipe busy |")
     print("|---|---|---|---|---|---|---|---|---|---|")
     for k in sorted(best):
@@ -46,4 +51,4 @@ def main(d):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1:])
