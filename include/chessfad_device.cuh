@@ -10,7 +10,9 @@
 //     };
 // written with the overloaded hDual<C> arithmetic (+ - * / with hDual or double operands,
 // sin cos exp sqrt log abs, comparisons on the value slot) of hdual.cuh (Fig. 1 rules,
-// PAPER.md:263-344).  y(k) returns the CHUNK-INIT seed of variable k (Alg 4) built on the fly.
+// PAPER.md:263-344).  y(k) returns the CHUNK-INIT seed of variable k (Alg 4) built on the fly,
+// as a seed-shaped chessfad::hs<C> (second-order slots structural zeros; every rule accepts it
+// and `hd<C> x = y(k);` converts it -- `auto x = y(k);` keeps the cheaper form, R7).
 // The functor runs inside the same lane=point / warp=row kernels as the built-in functions,
 // so the batched HVP (Alg 7), Hessian (Alg 5) and their symmetric variants (Alg 8, Alg 6)
 // are all available for it.  The functor object is passed by value as a kernel argument
