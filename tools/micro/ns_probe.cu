@@ -10,7 +10,13 @@
 
 using namespace chessfad;
 
-template <int FUNC, int NS, int C>
+// Ackley / Rosenbrock with the volatile-seed form forced on (policy experiments)
+template <int FUNC>
+struct VolOn : BuiltinFunc<FUNC> {
+  __host__ __device__ static constexpr bool vol_seeds(int, int, int) { return true; }
+};
+
+template <int FUNC, int NS, int C, class F = BuiltinFunc<FUNC>>
 void run(const char* name, int64_t m) {
   const int n = NS;
   std::vector<double> hp(m * n), hv(m * n);
@@ -24,7 +30,6 @@ void run(const char* name, int64_t m) {
   cudaMemcpy(dp, hp.data(), m * n * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(dv, hv.data(), m * n * 8, cudaMemcpyHostToDevice);
   BatchArgs a{n, C, 1, m, dp, dv, dout, nullptr, nullptr};
-  using F = BuiltinFunc<FUNC>;
   auto go = [&] { launch_functor<F, C, MODE_HVP, NS>(F{}, a, 0); };
   for (int w = 0; w < 2; w++) go();
   cudaEvent_t t0, t1;
@@ -44,6 +49,15 @@ void run(const char* name, int64_t m) {
 }
 
 int main() {
+  run<FUNC_ACKLEY, 16, 16>("ackley", 1048576);
+  run<FUNC_ACKLEY, 16, 16, VolOn<FUNC_ACKLEY>>("ackley-vol", 1048576);
+  run<FUNC_ACKLEY, 16, 8>("ackley", 1048576);
+  run<FUNC_ACKLEY, 16, 8, VolOn<FUNC_ACKLEY>>("ackley-vol", 1048576);
+  run<FUNC_ACKLEY, 8, 8>("ackley", 1048576);
+  run<FUNC_ACKLEY, 8, 8, VolOn<FUNC_ACKLEY>>("ackley-vol", 1048576);
+  run<FUNC_PRODSUM, 16, 16>("prodsum", 1048576);
+  run<FUNC_PRODSUM, 16, 16, VolOn<FUNC_PRODSUM>>("prodsum-vol", 1048576);
+  return 0;
   run<FUNC_ROSENBROCK, 16, 16>("rosenbrock", 1048576);
   run<FUNC_ACKLEY, 16, 16>("ackley", 1048576);
   run<FUNC_PRODSUM, 16, 16>("prodsum", 1048576);
