@@ -401,11 +401,12 @@ def test_sym_hvp_integer_bitwise(chf, func):
 
 
 @pytest.mark.parametrize("func", FUNCS)
-def test_sym_hessian_parity(chf, func):
+@pytest.mark.parametrize("n", [16, 32])
+def test_sym_hessian_parity(chf, func, n):
     """Alg 6 on the GPU: equals the oracle's Alg 6 within rounding, its computed (upper-chunk)
     entries equal the GPU's Alg 5 bit for bit, and it is exactly symmetric outside the
     diagonal chunks."""
-    n, m = 16, 150
+    m = 150 if n == 16 else 60
     P = synth.points(16, n, m)
     params = _params(func, n)
     dev = torch.device("cuda")
@@ -655,10 +656,11 @@ def test_paper_l2_baseline_parity(chf, func, n):
 
 # ------------------------------------------------------------ gradient by-product
 @pytest.mark.parametrize("func", FUNCS)
-def test_hessian_grad(chf, func):
+@pytest.mark.parametrize("n", [16, 32])
+def test_hessian_grad(chf, func, n):
     """grad from slot v[1] == the oracle's CHUNK-HESS gradient (and the Hessian is unchanged);
     Rosenbrock on integer inputs against its exact closed-form gradient, bit for bit."""
-    n, m = 16, 300
+    m = 300 if n == 16 else 100
     P = synth.points(19, n, m)
     params = _params(func, n)
     dev = torch.device("cuda")
