@@ -162,8 +162,12 @@ CHF_INL RowSink<MODE> make_sink(const BatchArgs& p, int i, int64_t e, const doub
 // constant; rows and chunks remain runtime loops, so every (row, chunk) evaluation of Alg 7 is
 // still formed from its own CHUNK-INIT seeds and executed on its own.  nvcc folds the seed
 // slots that become constants (x*1 -> x; IEEE-exact, outputs bit-identical to NS = 0).
+template <class F, int NS, int C, int MODE>
+__host__ __device__ constexpr int reg_min_blocks() {
+  return min_blocks_of<F>::get(NS, C, MODE) > 0 ? min_blocks_of<F>::get(NS, C, MODE) : CHF_REG_MINB;
+}
 template <class F, int C, int MODE, int W, int NS = 0>
-__global__ void __launch_bounds__(W * 32, CHF_REG_MINB) hvp_reg_kernel(BatchArgs p, F f) {
+__global__ void __launch_bounds__(W * 32, (reg_min_blocks<F, NS, C, MODE>())) hvp_reg_kernel(BatchArgs p, F f) {
   constexpr bool TRIG = uses_trig2pi<F>::value;
   constexpr bool HESS = mode_hess(MODE);
   extern __shared__ double smem[];

@@ -217,6 +217,9 @@ struct BuiltinFunc {
   // (n, kernel chunk C, mode)?  Measured (profiles/r02/ns3/summary.txt): faster for Rosenbrock
   // everywhere; for Ackley in the non-symmetric modes at n >= 32 with C >= 16 (n = 32 HVP 1.33x,
   // Hessian 1.25x; n = 64 also C <= 2); slower for prodsum.
+  __host__ __device__ static constexpr int min_blocks(int ns, int c, int mode) {
+    return (FUNC == FUNC_ACKLEY && ns == 16 && c == 16 && (mode == 0 || mode == 2)) ? 3 : 0;  // HVP modes
+  }
   __host__ __device__ static constexpr bool vol_seeds(int ns, int c, int mode) {
     return FUNC == FUNC_ROSENBROCK ||
            (FUNC == FUNC_ACKLEY && ns >= 32 && (c >= 16 || (ns == 64 && c <= 2)) &&
@@ -321,6 +324,19 @@ struct SparseFunc {
     else if constexpr (FUNC == FUNC_ACKLEY) return fsp_ackley<C>(n, y);
     else return fsp_prodsum<C>(n, y);
   }
+};
+
+// F::min_blocks(ns, c, mode): min resident CTAs per SM for the register kernel's launch bounds
+// (0 = the default CHF_REG_MINB); measured: Ackley compiled for n = 16 at C = 16 runs its HVP
+// modes 1-5% faster capped at 168 registers (3 CTAs/SM) but its Hessian 27% slower; every other
+// shape at its default (profiles/r02/ns3/, profiles/r02/a3/)
+template <class F, class = void>
+struct min_blocks_of {
+  __host__ __device__ static constexpr int get(int, int, int) { return 0; }
+};
+template <class F>
+struct min_blocks_of<F, decltype((void)F::min_blocks(0, 0, 0))> {
+  __host__ __device__ static constexpr int get(int ns, int c, int mode) { return F::min_blocks(ns, c, mode); }
 };
 
 // F::vol_seeds(ns, c, mode) if the functor declares it, else false (user functors)
