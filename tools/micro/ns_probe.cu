@@ -49,6 +49,9 @@ void run(const char* name, int64_t m) {
 }
 
 int main() {
+  run<FUNC_ROSENBROCK, 16, 16>("rosenbrock", 1048576);
+  run<FUNC_ROSENBROCK, 16, 8>("rosenbrock", 1048576);
+  run<FUNC_ROSENBROCK, 8, 8>("rosenbrock", 1048576);
   run<FUNC_ACKLEY, 16, 16>("ackley", 1048576);
   run<FUNC_ACKLEY, 16, 16, VolOn<FUNC_ACKLEY>>("ackley-vol", 1048576);
   run<FUNC_ACKLEY, 16, 8>("ackley", 1048576);
