@@ -45,3 +45,22 @@ extern "C" int user_batch(int algo, int n, int csize, long long m, const double*
 #undef CASE
   return -2;
 }
+
+// the same function through the kernels compiled for n = 16 (chessfad::user_batch_n, reading R8)
+extern "C" int user_batch_n16(int algo, int csize, long long m, const double* points, const double* vecs,
+                              double* out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  using namespace chessfad;
+#define CASE_N(C)                                                                                          \
+  case C:                                                                                                  \
+    switch (algo) {                                                                                        \
+      case 0: return (int)user_batch_n<16, C, USER_HVP>(UserF{}, 16, m, points, vecs, out, s);             \
+      case 1: return (int)user_batch_n<16, C, USER_HESSIAN>(UserF{}, 16, m, points, nullptr, out, s);      \
+      case 2: return (int)user_batch_n<16, C, USER_SYM_HVP>(UserF{}, 16, m, points, vecs, out, s);         \
+      case 3: return (int)user_batch_n<16, C, USER_SYM_HESSIAN>(UserF{}, 16, m, points, nullptr, out, s);  \
+    }                                                                                                      \
+    return -1;
+  switch (csize) { CASE_N(1) CASE_N(4) CASE_N(16) }
+#undef CASE_N
+  return -2;
+}

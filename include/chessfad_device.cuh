@@ -60,6 +60,34 @@ inline cudaError_t user_batch(const F& f, int n, int64_t m, const double* points
   return launch_functor<F, C, ALGO>(f, a, stream);
 }
 
+// The same kernels compiled for n == NS (reading R8; the paper's NV-templated kernels):
+// the functor's loops over the variables see a compile-time n, so nvcc can unroll them and fold
+// the seed's constant chunk slots; rows and chunks stay runtime loops (every evaluation is
+// executed on its own).  n must equal NS (cudaErrorInvalidValue otherwise).
+template <int NS, int C, int ALGO, class F>
+inline cudaError_t user_batch_n(const F& f, int n, int64_t m, const double* points, const double* vecs, double* out,
+                                cudaStream_t stream, double* grad = nullptr) {
+  static_assert(NS >= 1 && C >= 1 && NS % C == 0, "C must divide NS");
+  if (n != NS) return cudaErrorInvalidValue;
+  if (m < 0 || NS > 256) return cudaErrorInvalidValue;
+  if (m == 0) return cudaSuccess;
+  if (!points || !out || (!mode_hess(ALGO) && !vecs) || (ALGO == USER_HESSIAN_GRAD && !grad))
+    return cudaErrorInvalidValue;
+  if (reg_smem_bytes(uses_trig2pi<F>::value, n, groups_for(n, kWarpsReg, ALGO), ALGO) > 227 * 1024)
+    return cudaErrorInvalidValue;
+  BatchArgs a;
+  a.n = n;
+  a.csize = C;
+  a.groups = 1;
+  a.m = m;
+  a.points = points;
+  a.vecs = vecs;
+  a.out = out;
+  a.params = nullptr;
+  a.grad = grad;
+  return launch_functor<F, C, ALGO, NS>(f, a, stream);
+}
+
 // out[e*n+i] = sum_j d2f/dx_i dx_j (points[e]) vecs[e*n+j]     (Alg 7; USER_SYM_HVP: Alg 8)
 template <int C, class F>
 inline cudaError_t user_hvp_batch(const F& f, int n, int64_t m, const double* points, const double* vecs,

@@ -42,6 +42,8 @@ def userlib():
     vp = ctypes.c_void_p
     lib.user_batch.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_longlong, vp, vp, vp, vp]
     lib.user_batch.restype = ctypes.c_int
+    lib.user_batch_n16.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_longlong, vp, vp, vp, vp]
+    lib.user_batch_n16.restype = ctypes.c_int
     return lib
 
 
@@ -69,3 +71,33 @@ def test_user_function_all_algorithms(userlib):
             assert np.max(np.abs(Hg - Hs)) <= 1e-12 * np.abs(Hs).max(), (C, algo)
     out = torch.empty_like(p)
     assert userlib.user_batch(0, n, 3, m, p.data_ptr(), v.data_ptr(), out.data_ptr(), s) == -2  # C not compiled
+
+
+def test_user_function_compiled_n(userlib):
+    """chessfad::user_batch_n<16, C, ...> (the kernels compiled for n = 16, reading R8) against
+    the closed form and against the runtime-n kernels, every algorithm."""
+    n, m = 16, 700
+    P, V = synth.points(23, n, m), synth.vectors(23, n, m)
+    Hs = np.stack([closed_form_hessian(P[e]) for e in range(m)])
+    ref = np.einsum("eij,ej->ei", Hs, V)
+    scale = np.einsum("eij,ej->ei", np.abs(Hs), np.abs(V))
+    dev = torch.device("cuda")
+    p, v = torch.from_numpy(P).to(dev), torch.from_numpy(V).to(dev)
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for C in (1, 4, 16):
+        for algo in (0, 2):
+            out, out_rt = torch.empty_like(p), torch.empty_like(p)
+            assert userlib.user_batch_n16(algo, C, m, p.data_ptr(), v.data_ptr(), out.data_ptr(), s) == 0
+            assert userlib.user_batch(algo, n, C if C != 16 else 8, m, p.data_ptr(), v.data_ptr(),
+                                      out_rt.data_ptr(), s) == 0
+            torch.cuda.synchronize()
+            got = out.cpu().numpy()
+            err = np.abs(got - ref) / np.maximum(np.abs(ref), scale)
+            assert err.max() <= 1e-12, (C, algo, err.max())
+            err_rt = np.abs(got - out_rt.cpu().numpy()) / np.maximum(np.abs(ref), scale)
+            assert err_rt.max() <= 1e-12, (C, algo, err_rt.max())
+        for algo in (1, 3):
+            H = torch.empty((m, n, n), dtype=torch.float64, device=dev)
+            assert userlib.user_batch_n16(algo, C, m, p.data_ptr(), None, H.data_ptr(), s) == 0
+            torch.cuda.synchronize()
+            assert np.max(np.abs(H.cpu().numpy() - Hs)) <= 1e-12 * np.abs(Hs).max(), (C, algo)
