@@ -235,7 +235,8 @@ def hessian_batch_seedsparse(func, points, csize: int, params=None, out=None, st
 
 
 def sym_hvp_batch_seedsparse(func, points, vecs, csize: int, params=None, out=None, stream=None):
-    """Alg 8 with seed sparsity (F1/F2/F4): equals sym_hvp_batch up to the sign of zero."""
+    """Alg 8 with seed sparsity: equals sym_hvp_batch up to the sign of zero (F1/F2/F4), within
+    rounding of the tensor-core kernel for Fletcher-Powell (n <= 64)."""
     return _hvp("chessfad_sym_hvp_batch_seedsparse", func, points, vecs, csize, params, out, stream)
 
 

@@ -77,6 +77,11 @@ bool sparse_supported(int func, int n) {
   return n <= kMaxNF3 && f3_sparse_smem_bytes(n, groups_for(n, kWarpsF3, MODE_HVP)) <= kSmemMax;
 }
 
+// F3 seed-sparse Alg 8: every warp owns a 32-point group (4 groups per CTA) -> n <= 64
+bool f3_sparse_sym_hvp_fits(int n) {
+  return n <= kMaxNF3 && f3_sparse_smem_bytes(n, groups_for(n, kWarpsF3, MODE_SYM_HVP)) <= kSmemMax;
+}
+
 // register path: the chunk runs as column groups of the largest compiled c' (reg_kernel_chunk)
 template <int MODE>
 cudaError_t dispatch_sparse_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s) {
@@ -116,7 +121,8 @@ int sparse_entry(int func, int n, int csize, int64_t m, const double* points, co
   if (st) return st;
   if (MODE == MODE_HESS_GRAD && m > 0 && !grad) return CHESSFAD_ERR_ARG;
   if (!sparse_supported(func, n)) return CHESSFAD_ERR_UNSUPPORTED;
-  if (func == CHESSFAD_FLETCHER_POWELL && MODE == MODE_SYM_HVP) return CHESSFAD_ERR_UNSUPPORTED;
+  if (func == CHESSFAD_FLETCHER_POWELL && MODE == MODE_SYM_HVP && !f3_sparse_sym_hvp_fits(n))
+    return CHESSFAD_ERR_UNSUPPORTED;
   if (mode_sym(MODE) && func != CHESSFAD_FLETCHER_POWELL && !supported(func, n, csize, MODE))
     return CHESSFAD_ERR_UNSUPPORTED;
   if (m == 0) return CHESSFAD_OK;
@@ -600,9 +606,10 @@ int chessfad_is_supported_algo(int func, int n, int csize, int algo) {
                nullptr, nullptr))
     return 0;
   if (algo == CHESSFAD_ALGO_HVP_SEEDSPARSE || algo == CHESSFAD_ALGO_HESSIAN_SEEDSPARSE) return sparse_supported(func, n);
-  if (algo >= CHESSFAD_ALGO_SYM_HVP_SEEDSPARSE) {  // Fletcher-Powell: no seed-sparse Alg 8
+  if (algo >= CHESSFAD_ALGO_SYM_HVP_SEEDSPARSE) {  // Fletcher-Powell: seed-sparse Alg 8 up to n = 64
     static const int smode[3] = {MODE_SYM_HVP, MODE_SYM_HESS, MODE_HESS_GRAD};
-    if (func == CHESSFAD_FLETCHER_POWELL) return algo != CHESSFAD_ALGO_SYM_HVP_SEEDSPARSE && sparse_supported(func, n);
+    if (func == CHESSFAD_FLETCHER_POWELL)
+      return sparse_supported(func, n) && (algo != CHESSFAD_ALGO_SYM_HVP_SEEDSPARSE || f3_sparse_sym_hvp_fits(n));
     return sparse_supported(func, n) && supported(func, n, csize, smode[algo - CHESSFAD_ALGO_SYM_HVP_SEEDSPARSE]);
   }
   static const int mode_of[6] = {MODE_HVP, MODE_HESS, MODE_SYM_HVP, MODE_SYM_HESS, MODE_HVP_ROWHOIST, MODE_HESS_GRAD};

@@ -217,18 +217,25 @@ CHF_INL double f3_sp_diag(int n, int i, double si, double ci, const AB& ab,
 // hcol[col * n]; the unstaged path also skips the column blocks wholly below row i's chunk --
 // the staged path keeps every warp on the same block sequence for its shared barriers),
 // MODE_HESS_GRAD (stores the row and returns df/dx_i through f1).
+// MODE_SYM_HVP (Alg 8, one lane owns every row of its point): `acc` is the point's output row
+// (stride as), res starts from the mirror terms earlier rows scattered into acc[i], the direct
+// terms of chunks >= row i's chunk follow in ascending column order, and the entries of chunks
+// strictly after row i's are scattered into acc[col] (the register kernel's RowSink order).
 template <int CB, int MODE, bool STAGED, class AB>
 CHF_INL double f3_sp_row(int n, int Capi, int i, bool row0, const AB& ab, const double* __restrict__ sa,
                          const double* __restrict__ ca, const double* __restrict__ r0t, const double* __restrict__ v,
-                         int vs, double* __restrict__ hrow, double* __restrict__ hcol, const SpRing& rg, double& f1) {
+                         int vs, double* __restrict__ hrow, double* __restrict__ hcol, const SpRing& rg, double& f1,
+                         double* __restrict__ acc = nullptr, int as = 0) {
   constexpr bool HESS = mode_hess(MODE);
   constexpr bool GRAD = MODE == MODE_HESS_GRAD;
+  constexpr bool SYM = MODE == MODE_SYM_HESS || MODE == MODE_SYM_HVP;
   const double si = sa[i * kPad], ci = ca[i * kPad];
   const double fdiag = row0 ? f3_sp_diag<true, GRAD>(n, i, si, ci, ab, r0t, f1)
                             : f3_sp_diag<false, GRAD>(n, i, si, ci, ab, r0t, f1);
-  const int cs_row = (i / Capi) * Capi;  // first column of row i's chunk (Alg 6)
-  double res = 0.0;
-  const int cb_first = (MODE == MODE_SYM_HESS && !STAGED) ? cs_row / CB * CB : 0;
+  const int cs_row = (i / Capi) * Capi;  // first column of row i's chunk (Alg 6 / Alg 8)
+  double res = (MODE == MODE_SYM_HVP && acc) ? acc[i * as] : 0.0;
+  const double vi = MODE == MODE_SYM_HVP ? v[i * vs] : 0.0;
+  const int cb_first = (SYM && !STAGED) ? cs_row / CB * CB : 0;
   for (int cb = cb_first; cb < n; cb += CB) {
     double fC[CB];
     if constexpr (STAGED) {
@@ -252,6 +259,12 @@ CHF_INL double f3_sp_row(int n, int Capi, int i, bool row0, const AB& ab, const 
           }
         } else if (hrow) {
           hrow[col] = h;  // a7': H[e][i][col] (Alg 5)
+        }
+      } else if (MODE == MODE_SYM_HVP) {
+        const int col = cb + q;
+        if (col >= cs_row) {
+          res = __fma_rn(h, v[col * vs], res);                                  // Alg 8 :417-419
+          if (acc && col / Capi > i / Capi) acc[col * as] = __fma_rn(h, vi, acc[col * as]);  // :420-421
         }
       } else {
         res = __fma_rn(h, v[(cb + q) * vs], res);  // a5/a6: ascending columns, as RowSink
@@ -323,13 +336,29 @@ __global__ void __launch_bounds__(kWarpsF3 * 32, AB_SMEM ? CHF_SP_MINB_SMEM : CH
   const double* v = HESS ? nullptr : (SLIM ? p.vecs + ec * n : s_vec + g * n * kPad + lane);
   const int vs = SLIM ? 1 : kPad;
   double* o = s_out + g * n * kPad + lane;
+  // Alg 8 accumulators: the output tile column of the lane's point, or (SLIM) its output row in
+  // global memory (nullptr for a ragged-tail lane there: it computes but never accumulates)
+  double* acc = nullptr;
+  int as = 0;
+  if constexpr (MODE == MODE_SYM_HVP) {
+    if constexpr (SLIM) {
+      acc = e < p.m ? p.out + e * n : nullptr;
+      as = 1;
+    } else {
+      acc = o;
+      as = kPad;
+    }
+    if (acc)
+      for (int q = 0; q < n; q++) acc[q * as] = 0.0;
+  }
   // STAGED ring: [2][kSpKS][CB] shared block rows, then [warps][2][kSpKS] column values
   const SpRing rg{s_ab, s_ab + 2 * kSpKS * CB + warp * 2 * kSpKS};
   for (int i = wg; i < n; i += rstep) {
     double* hrow = (HESS && e < p.m) ? p.out + (e * n + i) * n : nullptr;
     double* hcol = (HESS && e < p.m) ? p.out + e * n * n + i : nullptr;
     double f1 = 0.0;
-    const double res = f3_sp_row<CB, MODE, STAGED>(n, p.csize, i, i == 0, ab, sa, ca, r0t, v, vs, hrow, hcol, rg, f1);
+    const double res =
+        f3_sp_row<CB, MODE, STAGED>(n, p.csize, i, i == 0, ab, sa, ca, r0t, v, vs, hrow, hcol, rg, f1, acc, as);
     if (MODE == MODE_HESS_GRAD && e < p.m) p.grad[e * n + i] = f1;
     if (HESS) {
     } else if (SLIM) {

@@ -52,7 +52,7 @@ inline size_t f3_sparse_smem_bytes(int n, int G) {
 }
 template <int CB, int MODE>
 cudaError_t launch_f3_sparse(BatchArgs a, cudaStream_t s) {
-  a.groups = groups_for(a.n, kWarpsF3, MODE_HVP);
+  a.groups = groups_for(a.n, kWarpsF3, MODE);  // Alg 8: every warp owns a group and walks all rows
   const int64_t P = 32 * a.groups;
   const int grid = (int)((a.m + P - 1) / P);
   const size_t smem = f3_sparse_smem_bytes(a.n, a.groups);
@@ -61,7 +61,8 @@ cudaError_t launch_f3_sparse(BatchArgs a, cudaStream_t s) {
                            : launch_with_smem(hvp_f3_sparse_kernel<CB, false, true, MODE, false>, grid, kWarpsF3 * 32, smem, s, a);
 }
 #define CHF_FOR_CB(X) X(1) X(2) X(4) X(8) X(16)
-#define CHF_FOR_F3SP_MODE(X, CB) X(CB, MODE_HVP) X(CB, MODE_HESS) X(CB, MODE_SYM_HESS) X(CB, MODE_HESS_GRAD)
+#define CHF_FOR_F3SP_MODE(X, CB) X(CB, MODE_HVP) X(CB, MODE_HESS) X(CB, MODE_SYM_HESS) X(CB, MODE_HESS_GRAD) \
+  X(CB, MODE_SYM_HVP)
 #define CHF_DECL_SP1(CB, M) extern template cudaError_t launch_f3_sparse<CB, M>(BatchArgs, cudaStream_t);
 #define CHF_DECL_SP(CB) CHF_FOR_F3SP_MODE(CHF_DECL_SP1, CB)
 CHF_FOR_CB(CHF_DECL_SP)

@@ -238,15 +238,19 @@ def test_device_header_self_contained(tmp_path):
 
 
 def test_seedsparse_symmetric_contract(lib):
-    """Seed-sparse Alg 8 / Alg 6 / gradient: every function except Alg 8 for Fletcher-Powell;
-    model = the algorithm's."""
+    """Seed-sparse Alg 8 / Alg 6 / gradient: every function (Alg 8 for Fletcher-Powell up to
+    n = 64); model = the algorithm's."""
     import paper_2410_22575_b200 as chf
     for algo in ("sym_hvp_seedsparse", "sym_hessian_seedsparse", "hessian_grad_seedsparse"):
         assert chf.is_supported("rosenbrock", 16, 4, algo)
-        assert chf.is_supported("fletcher_powell", 16, 4, algo) == (algo != "sym_hvp_seedsparse")
+        assert chf.is_supported("fletcher_powell", 16, 4, algo)
+        assert chf.is_supported("fletcher_powell", 64, 8, algo)
+    assert not chf.is_supported("fletcher_powell", 72, 8, "sym_hvp_seedsparse")
+    for algo in ("sym_hvp_seedsparse", "sym_hessian_seedsparse", "hessian_grad_seedsparse"):
         assert chf.path("ackley", 16, 4, algo) == "reg_seedsparse"
     assert chf.model_flops_per_point("rosenbrock", 16, 4, algo="sym_hvp_seedsparse") == \
         chf.model_flops_per_point("rosenbrock", 16, 4, algo="sym_hvp")
     vp = ctypes.c_void_p
     assert lib.chessfad_hessian_grad_batch_seedsparse(0, 16, 4, 10, vp(1), vp(1), None, None, None) == 1
-    assert lib.chessfad_sym_hvp_batch_seedsparse(2, 16, 4, 10, vp(1), vp(1), vp(1), vp(1), None) == 4
+    # Fletcher-Powell seed-sparse Alg 8 beyond n = 64: refused before anything is touched
+    assert lib.chessfad_sym_hvp_batch_seedsparse(2, 72, 8, 10, vp(1), vp(1), vp(1), vp(1), None) == 4

@@ -356,7 +356,7 @@ def test_f3_dmma_all_modes(chf, n, m):
 def test_seedsparse_sym_and_grad(chf, func, n, m):
     """Seed sparsity for Alg 8, Alg 6 and the gradient by-product (F1/F2/F4): the same values as
     the per-evaluation symmetric / gradient kernels (up to the sign of zero), and the oracle's
-    Alg 8 / Hessian / gradient; Fletcher-Powell is refused (ERR_UNSUPPORTED)."""
+    Alg 8 / Hessian / gradient.  (Fletcher-Powell: test_seedsparse_f3_sym_hvp.)"""
     P, V = synth.points(45, n, m), synth.vectors(45, n, m)
     dev = torch.device("cuda")
     p, v = torch.from_numpy(P).to(dev), torch.from_numpy(V).to(dev)
@@ -381,10 +381,32 @@ def test_seedsparse_sym_and_grad(chf, func, n, m):
         g_ref = np.stack([oracle.hessian(func, P[e], None, algo="chunk", C=C)[1] for e in range(4)])
         gs = np.abs(g_ref).max(axis=1, keepdims=True)
         assert (np.abs(gb.cpu().numpy()[:4] - g_ref) / gs).max() <= TIGHT
-    pr = torch.from_numpy(synth.fp_params_flat(0, n)).to(dev)
-    assert not chf.is_supported("fletcher_powell", n, 1, "sym_hvp_seedsparse")
+
+
+@pytest.mark.parametrize("n,m", [(6, 90), (16, 150), (32, 70), (40, 37), (64, 33)])
+def test_seedsparse_f3_sym_hvp(chf, n, m):
+    """Seed-sparse Alg 8 for Fletcher-Powell (every warp owns a 32-point group and walks all of
+    its rows; mirror terms accumulated in the output tile, or in the output row in global
+    memory for n > 32): the oracle's Alg 8 and Alg 7, and the tensor-core Alg 8 within rounding
+    (its E-sums associate differently, reading R6); ragged m; n > 64 is refused."""
+    func = "fletcher_powell"
+    P, V = synth.points(47, n, m), synth.vectors(47, n, m)
+    params = synth.fp_params_flat(0, n)
+    dev = torch.device("cuda")
+    p, v, pr = torch.from_numpy(P).to(dev), torch.from_numpy(V).to(dev), torch.from_numpy(params).to(dev)
+    ref7, sabs = oracle.hvp_batch(func, P, V, 1, params)
+    for C in sorted({1, 2, n // 2 if n // 2 <= 16 else 8, n}):
+        if n % C:
+            continue
+        assert chf.is_supported(func, n, C, "sym_hvp_seedsparse")
+        b = chf.sym_hvp_batch_seedsparse(func, p, v, C, pr).cpu().numpy()
+        _check(b, oracle.sc_hvp_batch(func, P, V, C, params), sabs)
+        _check(b, ref7, sabs)
+        _check(b, chf.sym_hvp_batch(func, p, v, C, pr).cpu().numpy(), sabs)
+    assert not chf.is_supported(func, 72, 8, "sym_hvp_seedsparse")
+    p72 = torch.zeros((2, 72), dtype=torch.float64, device=dev)
     with pytest.raises(chf.ChessfadError):
-        chf.sym_hvp_batch_seedsparse("fletcher_powell", p, v, 1, pr)
+        chf.sym_hvp_batch_seedsparse(func, p72, p72, 8, torch.from_numpy(synth.fp_params_flat(0, 72)).to(dev))
 
 
 @pytest.mark.parametrize("func", ["rosenbrock", "prodsum"])

@@ -33,7 +33,7 @@ def main():
     params = torch.from_numpy(synth.fp_params_flat(0, n)).to(dev)
     algo = args.algo or ("hessian" if args.hessian else "hvp")
     fn = {"hvp": chf.hvp_batch, "sym_hvp": chf.sym_hvp_batch, "hessian": chf.hessian_batch, "hvp_hoisted": chf.hvp_batch_hoisted, "hvp_seedsparse": chf.hvp_batch_seedsparse, "hessian_seedsparse": chf.hessian_batch_seedsparse,
-          "sym_hessian": chf.sym_hessian_batch}[algo]
+          "sym_hessian": chf.sym_hessian_batch, "sym_hvp_seedsparse": chf.sym_hvp_batch_seedsparse}[algo]
     for f in args.funcs:
         for c in args.csizes:
             if n % c or not chf.is_supported(f, n, c, algo):

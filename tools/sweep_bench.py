@@ -40,6 +40,7 @@ def main():
     Cs = args.csizes or [c for c in (1, 2, 4, 8, 16, 32, 64, 128) if c <= n and n % c == 0]
     hess = args.algo in ("hessian", "sym_hessian", "hessian_seedsparse")
     fn = {"hvp": chf.hvp_batch, "sym_hvp": chf.sym_hvp_batch, "hessian": chf.hessian_batch, "hvp_hoisted": chf.hvp_batch_hoisted, "hvp_seedsparse": chf.hvp_batch_seedsparse, "hessian_seedsparse": chf.hessian_batch_seedsparse,
+          "sym_hvp_seedsparse": chf.sym_hvp_batch_seedsparse,
           "sym_hessian": chf.sym_hessian_batch}[args.algo]
     for f in args.funcs:
         m = args.f3_m if (f == "fletcher_powell" and args.f3_m) else args.m
