@@ -224,15 +224,75 @@ def parse_args(argv):
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--ref-step-s", type=float, default=1.5, help="reference arm: seconds of oracle work per step")
     ap.add_argument("--sweep-out", default=os.path.join(ROOT, "gpurun_out", "bench_sweep.json"))
+    ap.add_argument("--cpu-ratio-vs-n", default=None, metavar="OUT.jsonl",
+                    help="only the paper's GPU-over-CPU quantity vs n (cpu_baseline leg per n), then exit")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
     return args
+
+
+def cpu_ratio_vs_n(out_path, funcs=("rosenbrock", "ackley", "fletcher_powell"), ns=(2, 4, 8, 16, 32, 64, 128),
+                   cpu_s=0.5):
+    """The paper's §VII quantity: per-point GPU time over per-point CPU time
+    as n grows, for the paper's three functions.  GPU: chessfad_hvp_batch at its best C over the
+    compiled set (inputs resident, CUDA events); CPU: the plain C oracle (Alg 7 as written, the
+    same C) on the host cores, a bounded sample (~cpu_s per (function, n)) -- the cpu_baseline
+    leg repeated per n.  One JSON line per (function, n) to out_path."""
+    import torch
+    import oracle
+    import paper_2410_22575_b200 as chf
+    dev = torch.device("cuda", 0)
+    oracle.build()
+    threads = oracle.default_threads()
+
+    def gpu_rate(func, n, C, m, pr):
+        p = torch.from_numpy(synth.points(0, n, m)).to(dev)
+        v = torch.from_numpy(synth.vectors(0, n, m)).to(dev)
+        out = torch.empty_like(p)
+        call = lambda: chf.hvp_batch(func, p, v, C, pr, out=out)  # noqa: E731
+        call()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        call()
+        torch.cuda.synchronize()
+        reps = max(2, min(50, int(0.2 / max(time.perf_counter() - t0, 1e-6))))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            call()
+        e1.record()
+        torch.cuda.synchronize()
+        return m / (e0.elapsed_time(e1) / reps * 1e-3)
+
+    with open(out_path, "w") as fo:
+        for f in funcs:
+            for n in ns:
+                pr_np = synth.fp_params_flat(0, n) if f == "fletcher_powell" else None
+                pr = None if pr_np is None else torch.from_numpy(pr_np).to(dev)
+                m = (1 << 20) if n <= 16 else (1 << 18) if n <= 64 else (1 << 16)
+                if f == "fletcher_powell":
+                    m = max(4096, m >> (4 if n >= 64 else 2))
+                best = None
+                for C in (c for c in (1, 2, 4, 8, 16, 32, 64, 128) if c <= n and n % c == 0):
+                    if chf.is_supported(f, n, C):
+                        r = gpu_rate(f, n, C, m, pr)
+                        if best is None or r > best[1]:
+                            best = (C, r)
+                C, g = best
+                c, m_cpu, dt = oracle_rate(f, n, C, pr_np, 0, cpu_s, threads)
+                fo.write(json.dumps({"func": f, "n": n, "C": C, "gpu_hvp_per_s": g, "gpu_m": m, "cpu_hvp_per_s": c,
+                                     "cpu_points": m_cpu, "cpu_s": dt, "cpu_threads": threads,
+                                     "gpu_over_cpu": g / c, "path": chf.path(f, n, C)}) + "\n")
+                fo.flush()
+    return 0
 
 
 def main(argv=None):
     if argv is None:
         argv = json.loads(os.environ["CHESSFAD_BENCH_ARGV"]) if "CHESSFAD_BENCH_ARGV" in os.environ else sys.argv[1:]
     args = parse_args(argv)
+    if args.cpu_ratio_vs_n:
+        return cpu_ratio_vs_n(args.cpu_ratio_vs_n)
     rc = maybe_respawn(args, argv)
     if rc is not None:
         return rc
