@@ -49,6 +49,13 @@ void run(const char* name, int64_t m) {
 }
 
 int main() {
+  if (getenv("NS_PROBE_BIG")) {
+    run<FUNC_ROSENBROCK, 128, 8>("rosenbrock", 65536);
+    run<FUNC_ROSENBROCK, 128, 16>("rosenbrock", 65536);
+    run<FUNC_ROSENBROCK, 64, 8>("rosenbrock", 262144);
+    run<FUNC_ROSENBROCK, 64, 16>("rosenbrock", 262144);
+    return 0;
+  }
   run<FUNC_ROSENBROCK, 16, 16>("rosenbrock", 1048576);
   run<FUNC_ROSENBROCK, 16, 8>("rosenbrock", 1048576);
   run<FUNC_ROSENBROCK, 8, 8>("rosenbrock", 1048576);
