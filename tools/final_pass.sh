@@ -13,3 +13,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 5 --warmup 3 --no-sweep --no-cpu --no-strong --e2e-steps 1 > $O/bench_ncu.log 2>&1; echo ncu_rc=$?
 python tools/launch_summary.py $O/launches.csv > $O/launches_summary.txt 2>&1
 tail -3 $O/pytest.log; tail -4 $O/smoke.log; tail -c 2000 $O/bench.log; echo; tail -1 $O/bench_reference.log; cat $O/launches_summary.txt
+python bench.py --cpu-ratio-vs-n $O/gpu_cpu_ratio.jsonl > $O/ratio.log 2>&1; echo ratio_rc=$?
