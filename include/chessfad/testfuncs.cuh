@@ -222,7 +222,7 @@ struct BuiltinFunc {
   }
   __host__ __device__ static constexpr bool vol_seeds(int ns, int c, int mode) {
     return FUNC == FUNC_ROSENBROCK ||
-           (FUNC == FUNC_ACKLEY && ns >= 32 && (c >= 16 || (ns == 64 && c <= 2)) &&
+           (FUNC == FUNC_ACKLEY && ns >= 32 && (c >= 16 || (ns == 64 && c <= 2) || (ns == 128 && c == 8)) &&
             mode != 2 && mode != 3);  // not MODE_SYM_HVP / MODE_SYM_HESS (kernels.cuh)
   }
   template <int C, class Seed>

@@ -195,14 +195,16 @@ bool stream_small_n(int func, int n, int C) {
 // runtime-n kernel).  n in {64, 128}, Alg 7 only (profiles/r02/ns/big_summary.txt,
 // profiles/r02/ns3/summary.txt): prodsum 2.4-10x at every C; Rosenbrock (volatile seeds,
 // unrolled chunks) at n = 64 every C (1.04-3.1x), at n = 128 C >= 4 (C = 1, 2 slower); Ackley
-// at n = 64 every C (1.1-1.6x; volatile seeds at C <= 2 and C >= 16) -- n = 128 spills.
+// at n = 64 every C (1.1-1.6x; volatile seeds at C <= 2 and C >= 16), at n = 128 kernel chunk 8
+// with volatile seeds (73.2 vs 79.3 ms per 2^16 points at the runtime kernel's best C;
+// profiles/r02/ns3/ns_probe_ack128.txt) -- its other chunks spill and run slower.
 #ifndef CHF_REGN_ALL
 #define CHF_REGN_ALL 0  // tuning: every compiled-n instantiation, measured or not
 #endif
 bool regn_use(int func, int n, int C, int mode) {
   if (!CHF_REGN) return false;
   if (CHF_REGN_ALL) {
-    if (n == 64 || n == 128) return mode == MODE_HVP && !(func == CHESSFAD_ACKLEY && n == 128);
+    if (n == 64 || n == 128) return mode == MODE_HVP;
     return n == 8 || n == 16 || n == 32;
   }
   if (n == 64 || n == 128) {
@@ -210,7 +212,7 @@ bool regn_use(int func, int n, int C, int mode) {
     switch (func) {
       case CHESSFAD_PRODSUM: return true;
       case CHESSFAD_ROSENBROCK: return n == 64 || C >= 4;
-      case CHESSFAD_ACKLEY: return n == 64;
+      case CHESSFAD_ACKLEY: return n == 64 || C == 8;  // n = 128: kernel chunk 8 only (1.08x)
     }
     return false;
   }
@@ -258,7 +260,7 @@ cudaError_t dispatch_reg(int func, int Capi, const BatchArgs& a, cudaStream_t s)
       if constexpr (MODE == MODE_HVP) {
         switch (func) {
           case CHESSFAD_ROSENBROCK: CHF_FOR_REGN_BIG_NS(CHF_CASE_NS, FUNC_ROSENBROCK) break;
-          case CHESSFAD_ACKLEY: CHF_CASE_NS(FUNC_ACKLEY, 64) break;
+          case CHESSFAD_ACKLEY: CHF_FOR_REGN_BIG_NS(CHF_CASE_NS, FUNC_ACKLEY) break;
           case CHESSFAD_PRODSUM: CHF_FOR_REGN_BIG_NS(CHF_CASE_NS, FUNC_PRODSUM) break;
         }
       }

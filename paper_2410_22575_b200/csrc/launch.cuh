@@ -32,12 +32,11 @@ CHF_FOR_REGN_NS(CHF_DECL_REGN0, FUNC_ROSENBROCK)
 CHF_FOR_REGN_NS(CHF_DECL_REGN0, FUNC_ACKLEY)
 CHF_FOR_REGN_NS(CHF_DECL_REGN0, FUNC_PRODSUM)
 // n in {64, 128}: Alg 7 only (cfg3 / cfg5); the other modes run the runtime-n kernel there
-// (Ackley: n = 64 only -- at n = 128 the unrolled kernel spills and measured slower)
 #define CHF_FOR_REGN_BIG_NS(X, F) X(F, 64) X(F, 128)
 #define CHF_DECL_REGNB1(F, C, NS) CHF_DECL_REGN2(F, C, MODE_HVP, NS)
 #define CHF_DECL_REGNB0(F, NS) CHF_FOR_REGN_C(CHF_DECL_REGNB1, F, NS)
 CHF_FOR_REGN_BIG_NS(CHF_DECL_REGNB0, FUNC_ROSENBROCK)
-CHF_DECL_REGNB0(FUNC_ACKLEY, 64)
+CHF_FOR_REGN_BIG_NS(CHF_DECL_REGNB0, FUNC_ACKLEY)
 CHF_FOR_REGN_BIG_NS(CHF_DECL_REGNB0, FUNC_PRODSUM)
 
 // NEXT-4 seed-sparse F3 HVP (f3_sparse.cuh): CB = column block, (A, B) in shared memory for

@@ -215,6 +215,7 @@ def test_kernel_path_introspection():
     assert chf.path("prodsum", 32, 4, "hessian") == "reg" and chf.path("rosenbrock", 32, 4, "hessian") == "reg_ns"
     assert chf.path("rosenbrock", 128, 2) == "reg" and chf.path("rosenbrock", 64, 1) == "reg_ns"
     assert chf.path("ackley", 128, 16) == "reg" and chf.path("ackley", 64, 64) == "reg_ns"
+    assert chf.path("ackley", 128, 8) == "reg_ns"
     assert chf.path("rosenbrock", 64, 16, "sym_hvp") == "reg" and chf.path("rosenbrock", 16, 16, "sym_hvp") == "reg_ns"
     assert chf.path("rosenbrock", 8, 2, "hvp_hoisted") == "small_hoisted"
     assert chf.path("rosenbrock", 3, 2) == "unsupported"

@@ -49,6 +49,12 @@ void run(const char* name, int64_t m) {
 }
 
 int main() {
+  if (getenv("NS_PROBE_ACK128")) {
+    run<FUNC_ACKLEY, 128, 16, VolOn<FUNC_ACKLEY>>("ackley-vol", 65536);
+    run<FUNC_ACKLEY, 128, 8, VolOn<FUNC_ACKLEY>>("ackley-vol", 65536);
+    run<FUNC_ACKLEY, 128, 16>("ackley", 65536);
+    return 0;
+  }
   if (getenv("NS_PROBE_BIG")) {
     run<FUNC_ROSENBROCK, 128, 8>("rosenbrock", 65536);
     run<FUNC_ROSENBROCK, 128, 16>("rosenbrock", 65536);
