@@ -255,3 +255,16 @@ def test_seedsparse_symmetric_contract(lib):
     assert lib.chessfad_hessian_grad_batch_seedsparse(0, 16, 4, 10, vp(1), vp(1), None, None, None) == 1
     # Fletcher-Powell seed-sparse Alg 8 beyond n = 64: refused before anything is touched
     assert lib.chessfad_sym_hvp_batch_seedsparse(2, 72, 8, 10, vp(1), vp(1), vp(1), vp(1), None) == 4
+
+
+def test_seed_type_rules_compile(tmp_path):
+    """Reading R7 at the type level: the result types of every hDual rule with seed-shaped
+    operands (static_asserts in tests/cuda/seed_type_rules.cu; compile-only, no GPU)."""
+    import shutil
+    import subprocess
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-std=c++17", "-O1", "-I",
+                        os.path.join(root, "include"), "-c", os.path.join(root, "tests", "cuda", "seed_type_rules.cu"),
+                        "-o", str(tmp_path / "rules.o")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
